@@ -1,0 +1,149 @@
+/* vecattn.h — C ABI of the B200 (sm_100a) VecAttention hot path.
+ *
+ * VecAttention (arXiv 2603.29494, /root/reference/PAPER.md = "P:<line>"):
+ *   stage 1  important-vector selection: query pooling (Eq. 2) +
+ *            TilingSelect with the minS filter (Eq. 3; Sec. 3.1.3
+ *            P:268-307; Alg. 1) -> per-query-block sorted key indices;
+ *   stage 2  vector-sparse attention (Eq. 5; Alg. 2);
+ *   plus     dense attention (Eq. 1) as the in-library reference kernel.
+ *
+ * Conventions (all entry points):
+ *  - Every tensor pointer is a DEVICE pointer (cudaMalloc / torch CUDA memory),
+ *    16-byte aligned.  bf16 = IEEE bfloat16 bit patterns.  Layouts are dense,
+ *    row-major:  Q [B, Hq, N, D],  K, V [B, Hkv, N, D],  O [B, Hq, N, D],
+ *    LSE [B, Hq, N] fp32 (natural log).  GQA: query head h reads KV head
+ *    h / (Hq / Hkv) (reading R13).
+ *  - All work is enqueued asynchronously on `stream`; nothing is synchronised.
+ *  - Ownership: the caller owns every buffer, including the workspace `ws`
+ *    (size from the matching *_workspace_bytes()).  The library never allocates.
+ *  - Errors: argument/shape problems return a status synchronously BEFORE any
+ *    launch (no side effects).  Device faults surface at the caller's next sync as
+ *    CUDA errors.  VECATTN_ERR_CUDA means a launch failed; cudaGetLastError() is
+ *    left set.
+ *  - Selection output is CSR over query blocks.  Row id r = (b*Hq + h)*N_p + i,
+ *    N_p = ceil(N / pq).  offsets: int64 [B*Hq*N_p + 1], indices: int32 [nnz],
+ *    ascending and unique within a row, each in [0, N), and <= L_i =
+ *    min(N,(i+1)*pq)-1 when causal (reading R5).
+ */
+#ifndef VECATTN_H
+#define VECATTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define VECATTN_API __attribute__((visibility("default")))
+#else
+#define VECATTN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* vecattn_stream_t; /* ABI-identical to cudaStream_t; NULL = legacy stream */
+
+typedef enum {
+    VECATTN_OK = 0,
+    VECATTN_ERR_INVALID_ARGUMENT = 1, /* NULL pointer, pq not in {64,128}, alpha < 0 or NaN, bk not in
+                                         {16,32,64}, gk < 1, TOPK with neither topk > 0 nor
+                                         keep_frac in (0,1], Hq % Hkv != 0, scale < 0 or NaN          */
+    VECATTN_ERR_SHAPE = 2,            /* B, N < 1; D not in {64,128}; N >= 2^30; Hq > 1024; pointer not
+                                         16-byte aligned; B*Hkv*N >= 2^31                              */
+    VECATTN_ERR_UNSUPPORTED = 3,      /* no sm_100 device, or cuTensorMapEncodeTiled unavailable      */
+    VECATTN_ERR_WORKSPACE = 4,        /* ws == NULL or ws_bytes < *_workspace_bytes()                 */
+    VECATTN_ERR_CUDA = 5              /* a CUDA launch/API call failed                                */
+} vecattn_status_t;
+
+/* Problem statement (north_star: Q/K/V [B,H,N,d] bf16, causal flag). */
+typedef struct {
+    int64_t B, Hq, Hkv, N, D;
+    int32_t causal;  /* 1 = VLM prefill (key j visible to query r iff j <= r); 0 = DiT     */
+    float scale;     /* softmax scale tau; 0 => 1/sqrt(D) (Eq. 1; Alg. 2 line P:870) */
+} vecattn_problem_t;
+
+typedef enum {
+    VECATTN_SEL_MINS_ALG1 = 0,  /* Alg. 1 exactly: running row max over B_K-key tiles, reset every
+                                   G_K tiles, keep s >= m - alpha (readings R1-R3)          */
+    VECATTN_SEL_MINS_EXACT = 1, /* Eq. 3 with the global row max (two GEMM passes)                  */
+    VECATTN_SEL_TOPK = 2        /* per-block budget k_i, ties -> lowest index (R12)      */
+} vecattn_sel_mode_t;
+
+typedef struct {
+    int32_t mode;                /* vecattn_sel_mode_t                                              */
+    int32_t pq;                  /* vector size P_q = query-block size, 64 or 128   */
+    int32_t bk;                  /* Alg. 1 K-tile size B_K: 16, 32 or 64 (paper default 16)         */
+    int32_t gk;                  /* Alg. 1 K-tiles per group G_K >= 1 (16 VLM, 8192 DiT)     */
+    float alpha;                 /* minS filtering ratio (Eq. 3), >= 0, in scaled-logit units (R4)  */
+    const float* alpha_per_head; /* HOST pointer [Hq] or NULL; overrides alpha per query head (Eq. 4) */
+    int64_t topk;                /* TOPK: k_i = min(topk, |V_i|) when topk > 0, else ...             */
+    float keep_frac;             /* ... k_i = clamp(floor(keep_frac*|V_i| + 0.5), 1, |V_i|)         */
+} vecattn_select_params_t;
+
+/* ---------------------------------------------------------------- stage 1 */
+
+/* Eq. 2: qp [B,Hq,N_p,D] bf16 = RNE-bf16 of the exact fp64 block mean
+ * (ragged last block: its true height, reading R7).  q, qp: device.              */
+VECATTN_API vecattn_status_t vecattn_pool(const vecattn_problem_t* p, int32_t pq, const void* q, void* qp,
+                              vecattn_stream_t stream);
+
+VECATTN_API size_t vecattn_select_workspace_bytes(const vecattn_problem_t* p, const vecattn_select_params_t* s);
+
+/* Important-vector selection (Alg. 1).  Writes `offsets` (always),
+ * `*d_nnz` (device int64, always) and, iff indices != NULL and nnz <= cap, the
+ * ascending `indices`.  Capacity protocol: if nnz > cap the contents of indices are
+ * unspecified; read d_nnz, re-allocate and call again (indices = NULL, cap = 0 is a
+ * counts-only call, e.g. for alpha calibration).  The estimated attention map is
+ * never written to memory: scores live in TMEM, only a 1-bit mask per (block, key)
+ * reaches HBM (workspace).                                                          */
+VECATTN_API vecattn_status_t vecattn_select(const vecattn_problem_t* p, const vecattn_select_params_t* s,
+                                const void* q, const void* k, int64_t* offsets, int32_t* indices,
+                                int64_t cap, int64_t* d_nnz, void* ws, size_t ws_bytes,
+                                vecattn_stream_t stream);
+
+/* ---------------------------------------------------------------- stage 2 */
+
+VECATTN_API size_t vecattn_sparse_workspace_bytes(const vecattn_problem_t* p, int32_t pq, int64_t nnz_cap);
+
+/* Vector-sparse attention, Eq. 5 / Alg. 2: for every query
+ * block i, O[rows of i] = softmax(scale * Q[rows] K[Idx(i)]^T) V[Idx(i)], causal rows
+ * additionally masked to keys j <= r.  A row with no visible selected key outputs
+ * O_r = V_r and LSE_r = scale*<q_r,k_r> (reading R6).  offsets/indices: CSR as
+ * produced by vecattn_select (same pq); nnz = offsets[last] must be <= nnz_cap.
+ * Index content is NOT validated (O(nnz)); out-of-range indices are undefined
+ * behaviour -- see vecattn_validate_selection.  lse may be NULL.                    */
+VECATTN_API vecattn_status_t vecattn_sparse_fwd(const vecattn_problem_t* p, int32_t pq, const void* q, const void* k,
+                                    const void* v, const int64_t* offsets, const int32_t* indices,
+                                    int64_t nnz_cap, void* o, float* lse, void* ws, size_t ws_bytes,
+                                    vecattn_stream_t stream);
+
+/* ------------------------------------------------------------- reference */
+
+VECATTN_API size_t vecattn_dense_workspace_bytes(const vecattn_problem_t* p);
+
+/* Dense attention, Eq. 1, same kernel skeleton with contiguous K/V tiles
+ * (the speed-up denominator).  lse may be NULL.                                     */
+VECATTN_API vecattn_status_t vecattn_dense_fwd(const vecattn_problem_t* p, const void* q, const void* k, const void* v,
+                                   void* o, float* lse, void* ws, size_t ws_bytes, vecattn_stream_t stream);
+
+/* ----------------------------------------------------------- diagnostics */
+
+/* Test hook: writes d_bad[0] = number of CSR rows violating ascending/unique/range/
+ * causal rules (device int32).                                                      */
+VECATTN_API vecattn_status_t vecattn_validate_selection(const vecattn_problem_t* p, int32_t pq, const int64_t* offsets,
+                                            const int32_t* indices, int32_t* d_bad, vecattn_stream_t stream);
+
+/* Test hook: the raw pooled-score accumulators <Q_p[i], k_j> (fp32, unscaled) of the
+ * selection GEMM, scores [B*Hq*N_p, N]; ws sized by vecattn_select_workspace_bytes
+ * with the same pq.                                                                  */
+VECATTN_API vecattn_status_t vecattn_debug_scores(const vecattn_problem_t* p, int32_t pq, const void* q, const void* k,
+                                      float* scores, void* ws, size_t ws_bytes, vecattn_stream_t stream);
+
+VECATTN_API const char* vecattn_status_string(vecattn_status_t s);
+VECATTN_API int32_t vecattn_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VECATTN_H */

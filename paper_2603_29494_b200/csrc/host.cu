@@ -1,0 +1,428 @@
+// host.cu — the C ABI (include/vecattn.h): argument validation, workspace
+// carving, TMA tensor-map encoding and kernel launches.  No compute happens here:
+// every step of the path runs in the kernels of pool.cu / select.cu / compact.cu /
+// attn.cu.
+#include "../../include/vecattn.h"
+#include "kernels.cuh"
+
+#include <cudaTypedefs.h>
+#include <math.h>
+#include <mutex>
+#include <string.h>
+
+namespace {
+
+using va::AttnParams;
+using va::SelectParams;
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+    std::call_once(g_encode_once, [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    });
+    return g_encode;
+}
+
+// bf16 tensor [d2][d1][d0] (d0 innermost), box {64, box1, 1}, 128B swizzle, OOB -> 0.
+bool tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t box1) {
+    auto enc = encoder();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {d0, d1, d2};
+    cuuint64_t strides[2] = {d0 * 2, d0 * d1 * 2};
+    cuuint32_t box[3] = {64, box1, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// bf16 rows [rows][d0], box {64, 1} for tile::gather4 (4 rows per instruction).
+bool tmap_gather(CUtensorMap* m, const void* base, uint64_t d0, uint64_t rows) {
+    auto enc = encoder();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {d0, rows};
+    cuuint64_t strides[1] = {d0 * 2};
+    cuuint32_t box[2] = {64, 1};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool aligned16(const void* ptr) { return ((uintptr_t)ptr & 15u) == 0; }
+
+vecattn_status_t check_problem(const vecattn_problem_t* p) {
+    if (!p) return VECATTN_ERR_INVALID_ARGUMENT;
+    if (p->B < 1 || p->Hq < 1 || p->Hkv < 1 || p->N < 1) return VECATTN_ERR_SHAPE;
+    if (p->D != 64 && p->D != 128) return VECATTN_ERR_SHAPE;
+    if (p->N >= (int64_t(1) << 30) || p->Hq > 1024) return VECATTN_ERR_SHAPE;
+    if (p->B * p->Hkv * p->N >= (int64_t(1) << 31) || p->B * p->Hq * p->N >= (int64_t(1) << 31))
+        return VECATTN_ERR_SHAPE;
+    if (p->Hq % p->Hkv != 0) return VECATTN_ERR_INVALID_ARGUMENT;
+    if (!(p->scale >= 0.f) || isinf(p->scale)) return VECATTN_ERR_INVALID_ARGUMENT;
+    return VECATTN_OK;
+}
+
+float eff_scale(const vecattn_problem_t* p) { return p->scale > 0.f ? p->scale : 1.0f / sqrtf((float)p->D); }
+
+int64_t n_pooled(const vecattn_problem_t* p, int32_t pq) { return (p->N + pq - 1) / pq; }
+
+int64_t words_per_row(const vecattn_problem_t* p) { return (p->N + 255) / 256 * 8; }
+
+vecattn_status_t check_select(const vecattn_problem_t* p, const vecattn_select_params_t* s) {
+    vecattn_status_t st = check_problem(p);
+    if (st != VECATTN_OK) return st;
+    if (!s) return VECATTN_ERR_INVALID_ARGUMENT;
+    if (s->pq != 64 && s->pq != 128) return VECATTN_ERR_INVALID_ARGUMENT;
+    if (s->mode < 0 || s->mode > 2) return VECATTN_ERR_INVALID_ARGUMENT;
+    if (s->mode == VECATTN_SEL_MINS_ALG1 && s->bk != 16 && s->bk != 32 && s->bk != 64)
+        return VECATTN_ERR_INVALID_ARGUMENT;
+    if (s->mode == VECATTN_SEL_MINS_ALG1 && s->gk < 1) return VECATTN_ERR_INVALID_ARGUMENT;
+    if (s->mode != VECATTN_SEL_TOPK) {
+        if (!(s->alpha >= 0.f) || isinf(s->alpha)) return VECATTN_ERR_INVALID_ARGUMENT;
+        if (s->alpha_per_head)
+            for (int64_t h = 0; h < p->Hq; ++h)
+                if (!(s->alpha_per_head[h] >= 0.f) || isinf(s->alpha_per_head[h])) return VECATTN_ERR_INVALID_ARGUMENT;
+    } else {
+        if (s->topk <= 0 && !(s->keep_frac > 0.f && s->keep_frac <= 1.f)) return VECATTN_ERR_INVALID_ARGUMENT;
+    }
+    return VECATTN_OK;
+}
+
+struct SelectWs {
+    void* qp;
+    uint32_t* bitmask;
+    unsigned long long* counts;
+    uint32_t* rowmax;
+    uint32_t* tk_prefix;
+    uint32_t* tk_krem;
+    size_t total;
+};
+
+SelectWs carve_select(const vecattn_problem_t* p, int32_t pq, void* base) {
+    const int64_t BH = p->B * p->Hq, Np = n_pooled(p, pq), R = BH * Np;
+    uint8_t* b = static_cast<uint8_t*>(base);
+    size_t off = 0;
+    SelectWs w;
+    w.qp = b + off;
+    off += align_up((size_t)R * p->D * 2);
+    w.bitmask = reinterpret_cast<uint32_t*>(b + off);
+    off += align_up((size_t)R * words_per_row(p) * 4);
+    w.counts = reinterpret_cast<unsigned long long*>(b + off);
+    off += align_up((size_t)R * 8);
+    w.rowmax = reinterpret_cast<uint32_t*>(b + off);
+    off += align_up((size_t)R * 4);
+    w.tk_prefix = reinterpret_cast<uint32_t*>(b + off);
+    off += align_up((size_t)R * 4);
+    w.tk_krem = reinterpret_cast<uint32_t*>(b + off);
+    off += align_up((size_t)R * 4);
+    w.total = off;
+    return w;
+}
+
+int64_t gcd64(int64_t a, int64_t b) { return b == 0 ? a : gcd64(b, a % b); }
+
+// Keys per CTA unit.  Units never split a G_K group (Alg. 1 running max scope), so a
+// segment is a multiple of lcm(B_K*G_K, 256); TOPK needs whole rows.
+void plan_segments(const vecattn_problem_t* p, const vecattn_select_params_t* s, int epi, SelectParams& sp) {
+    const int64_t Nr = (p->N + 255) / 256 * 256;
+    int64_t seg = Nr;
+    if (epi == va::EPI_ALG1) {
+        const int64_t G = (int64_t)s->bk * (int64_t)s->gk;
+        if (G < p->N) {
+            const int64_t L = G / gcd64(G, 256) * 256;
+            if (L < p->N) seg = L * std::max<int64_t>(1, 16384 / L);
+        }
+    } else if (epi == va::EPI_MAX || epi == va::EPI_THRESH || epi == va::EPI_SCORES) {
+        seg = 16384;
+    }
+    if (seg > Nr) seg = Nr;
+    sp.seg_len = seg;
+    sp.n_seg = (p->N + seg - 1) / seg;
+}
+
+vecattn_status_t fill_select_params(const vecattn_problem_t* p, const vecattn_select_params_t* s, int32_t pq,
+                                    const void* k, const SelectWs& w, SelectParams& sp) {
+    memset(&sp, 0, sizeof(sp));
+    const int64_t BH = p->B * p->Hq, Np = n_pooled(p, pq);
+    sp.N = p->N;
+    sp.Np = Np;
+    sp.BH = BH;
+    sp.Hq = p->Hq;
+    sp.Hkv = p->Hkv;
+    sp.pq = pq;
+    sp.causal = p->causal ? 1 : 0;
+    sp.bk = s ? s->bk : 16;
+    sp.gk = s ? s->gk : 1;
+    sp.n_mt = (Np + 127) / 128;
+    sp.words_per_row = words_per_row(p);
+    sp.bitmask = w.bitmask;
+    sp.counts = w.counts;
+    sp.rowmax = w.rowmax;
+    sp.tk_prefix = w.tk_prefix;
+    sp.tk_krem = w.tk_krem;
+    sp.topk = s ? s->topk : 0;
+    sp.keep_frac = s ? s->keep_frac : 0.f;
+    const float scale = eff_scale(p);
+    for (int64_t h = 0; h < p->Hq; ++h) {
+        const float a = s ? (s->alpha_per_head ? s->alpha_per_head[h] : s->alpha) : 0.f;
+        sp.alpha_raw[h] = a / scale;
+    }
+    if (!tmap_3d(&sp.tm_qp, w.qp, (uint64_t)p->D, (uint64_t)Np, (uint64_t)BH, 128)) return VECATTN_ERR_UNSUPPORTED;
+    return VECATTN_OK;
+}
+
+vecattn_status_t set_k_map(const vecattn_problem_t* p, const void* k, int bn, SelectParams& sp) {
+    if (!tmap_3d(&sp.tm_k, k, (uint64_t)p->D, (uint64_t)p->N, (uint64_t)(p->B * p->Hkv), (uint32_t)bn))
+        return VECATTN_ERR_UNSUPPORTED;
+    return VECATTN_OK;
+}
+
+#define VA_CU(x)                                       \
+    do {                                               \
+        if ((x) != cudaSuccess) return VECATTN_ERR_CUDA; \
+    } while (0)
+
+__global__ void validate_kernel(const int64_t* __restrict__ offsets, const int32_t* __restrict__ indices,
+                                int64_t R, int64_t Np, int64_t N, int32_t pq, int32_t causal, int32_t* d_bad) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= R) return;
+    const int64_t i = r % Np;
+    const int64_t lim = causal ? std::min<int64_t>(N, (i + 1) * (int64_t)pq) : N;  // exclusive
+    const int64_t a = offsets[r], b = offsets[r + 1];
+    bool bad = b < a;
+    int64_t prev = -1;
+    for (int64_t t = a; t < b && !bad; ++t) {
+        const int64_t j = indices[t];
+        if (j <= prev || j < 0 || j >= lim) bad = true;
+        prev = j;
+    }
+    if (bad) atomicAdd(d_bad, 1);
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t vecattn_abi_version(void) { return 1; }
+
+const char* vecattn_status_string(vecattn_status_t s) {
+    switch (s) {
+        case VECATTN_OK: return "ok";
+        case VECATTN_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case VECATTN_ERR_SHAPE: return "unsupported or invalid shape";
+        case VECATTN_ERR_UNSUPPORTED: return "unsupported device or driver";
+        case VECATTN_ERR_WORKSPACE: return "workspace too small";
+        case VECATTN_ERR_CUDA: return "CUDA launch error";
+    }
+    return "unknown status";
+}
+
+vecattn_status_t vecattn_pool(const vecattn_problem_t* p, int32_t pq, const void* q, void* qp,
+                              vecattn_stream_t stream) {
+    vecattn_status_t st = check_problem(p);
+    if (st != VECATTN_OK) return st;
+    if (pq != 64 && pq != 128) return VECATTN_ERR_INVALID_ARGUMENT;
+    if (!q || !qp) return VECATTN_ERR_INVALID_ARGUMENT;
+    if (!aligned16(q) || !aligned16(qp)) return VECATTN_ERR_SHAPE;
+    VA_CU(va::launch_pool(q, qp, p->B * p->Hq, p->N, p->D, pq, (cudaStream_t)stream));
+    return VECATTN_OK;
+}
+
+size_t vecattn_select_workspace_bytes(const vecattn_problem_t* p, const vecattn_select_params_t* s) {
+    if (check_problem(p) != VECATTN_OK || !s || (s->pq != 64 && s->pq != 128)) return 0;
+    return carve_select(p, s->pq, nullptr).total;
+}
+
+vecattn_status_t vecattn_select(const vecattn_problem_t* p, const vecattn_select_params_t* s, const void* q,
+                                const void* k, int64_t* offsets, int32_t* indices, int64_t cap, int64_t* d_nnz,
+                                void* ws, size_t ws_bytes, vecattn_stream_t stream) {
+    vecattn_status_t st = check_select(p, s);
+    if (st != VECATTN_OK) return st;
+    if (!q || !k || !offsets || !d_nnz || cap < 0 || (cap > 0 && !indices)) return VECATTN_ERR_INVALID_ARGUMENT;
+    if (!aligned16(q) || !aligned16(k)) return VECATTN_ERR_SHAPE;
+    const SelectWs need = carve_select(p, s->pq, nullptr);
+    if (!ws || ws_bytes < need.total) return VECATTN_ERR_WORKSPACE;
+    if (!aligned16(ws)) return VECATTN_ERR_SHAPE;
+    cudaStream_t cs = (cudaStream_t)stream;
+    const SelectWs w = carve_select(p, s->pq, ws);
+    SelectParams* sp = new SelectParams;
+    st = fill_select_params(p, s, s->pq, k, w, *sp);
+    if (st != VECATTN_OK) { delete sp; return st; }
+    const int64_t R = sp->BH * sp->Np;
+    auto run = [&](int epi, int pass) -> cudaError_t {
+        plan_segments(p, s, epi, *sp);
+        sp->pass = pass;
+        if (set_k_map(p, k, epi == va::EPI_TOPK_HIST ? 128 : 256, *sp) != VECATTN_OK) return cudaErrorInvalidValue;
+        return va::launch_select(*sp, epi, (int)p->D, cs);
+    };
+    cudaError_t e = va::launch_pool(q, w.qp, sp->BH, p->N, p->D, s->pq, cs);
+    if (e == cudaSuccess) e = cudaMemsetAsync(w.counts, 0, (size_t)R * 8, cs);
+    if (e == cudaSuccess) {
+        if (s->mode == VECATTN_SEL_MINS_ALG1) {
+            e = run(va::EPI_ALG1, 0);
+        } else if (s->mode == VECATTN_SEL_MINS_EXACT) {
+            e = cudaMemsetAsync(w.rowmax, 0, (size_t)R * 4, cs);
+            if (e == cudaSuccess) e = run(va::EPI_MAX, 0);
+            if (e == cudaSuccess) e = run(va::EPI_THRESH, 0);
+        } else {
+            for (int pass = 0; pass < 4 && e == cudaSuccess; ++pass) e = run(va::EPI_TOPK_HIST, pass);
+            if (e == cudaSuccess) e = run(va::EPI_TOPK_EMIT, 0);
+        }
+    }
+    if (e == cudaSuccess) e = va::launch_scan(w.counts, R, offsets, d_nnz, cs);
+    if (e == cudaSuccess && indices && cap > 0)
+        e = va::launch_emit(w.bitmask, sp->words_per_row, offsets, d_nnz, cap, indices, sp->BH, sp->Np, p->N,
+                            s->pq, p->causal ? 1 : 0, cs);
+    delete sp;
+    return e == cudaSuccess ? VECATTN_OK : VECATTN_ERR_CUDA;
+}
+
+vecattn_status_t vecattn_debug_scores(const vecattn_problem_t* p, int32_t pq, const void* q, const void* k,
+                                      float* scores, void* ws, size_t ws_bytes, vecattn_stream_t stream) {
+    vecattn_status_t st = check_problem(p);
+    if (st != VECATTN_OK) return st;
+    if ((pq != 64 && pq != 128) || !q || !k || !scores) return VECATTN_ERR_INVALID_ARGUMENT;
+    const SelectWs need = carve_select(p, pq, nullptr);
+    if (!ws || ws_bytes < need.total) return VECATTN_ERR_WORKSPACE;
+    cudaStream_t cs = (cudaStream_t)stream;
+    const SelectWs w = carve_select(p, pq, ws);
+    vecattn_select_params_t s;
+    memset(&s, 0, sizeof(s));
+    s.pq = pq;
+    s.bk = 16;
+    s.gk = 1;
+    SelectParams* sp = new SelectParams;
+    st = fill_select_params(p, &s, pq, k, w, *sp);
+    if (st == VECATTN_OK) st = set_k_map(p, k, 256, *sp);
+    if (st != VECATTN_OK) { delete sp; return st; }
+    sp->scores_out = scores;
+    plan_segments(p, &s, va::EPI_SCORES, *sp);
+    cudaError_t e = va::launch_pool(q, w.qp, sp->BH, p->N, p->D, pq, cs);
+    if (e == cudaSuccess) e = va::launch_select(*sp, va::EPI_SCORES, (int)p->D, cs);
+    delete sp;
+    return e == cudaSuccess ? VECATTN_OK : VECATTN_ERR_CUDA;
+}
+
+size_t vecattn_sparse_workspace_bytes(const vecattn_problem_t* p, int32_t pq, int64_t nnz_cap) {
+    if (check_problem(p) != VECATTN_OK || (pq != 64 && pq != 128) || nnz_cap < 0) return 0;
+    const int64_t n_mt = (p->N + 127) / 128;
+    return align_up((size_t)nnz_cap * 4) + align_up((size_t)(p->B * p->Hq * n_mt) * 4) + kAlign;
+}
+
+static vecattn_status_t attn_common(const vecattn_problem_t* p, const void* q, const void* k, const void* v,
+                                    void* o, float* lse, AttnParams& ap) {
+    memset(&ap, 0, sizeof(ap));
+    const float scale = eff_scale(p);
+    ap.q = (const __nv_bfloat16*)q;
+    ap.k = (const __nv_bfloat16*)k;
+    ap.v = (const __nv_bfloat16*)v;
+    ap.o = (__nv_bfloat16*)o;
+    ap.lse = lse;
+    ap.N = p->N;
+    ap.BH = p->B * p->Hq;
+    ap.Hq = p->Hq;
+    ap.Hkv = p->Hkv;
+    ap.n_mt = (p->N + 127) / 128;
+    ap.total_items = ap.BH * ap.n_mt;
+    ap.causal = p->causal ? 1 : 0;
+    ap.scale = scale;
+    ap.scale_log2 = scale * 1.4426950408889634f;
+    if (!tmap_3d(&ap.tm_q, q, (uint64_t)p->D, (uint64_t)p->N, (uint64_t)ap.BH, 128)) return VECATTN_ERR_UNSUPPORTED;
+    return VECATTN_OK;
+}
+
+static int attn_grid(int64_t items) {
+    int dev = 0, sms = va::kNumSMsB200;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(items, sms));
+}
+
+vecattn_status_t vecattn_sparse_fwd(const vecattn_problem_t* p, int32_t pq, const void* q, const void* k,
+                                    const void* v, const int64_t* offsets, const int32_t* indices, int64_t nnz_cap,
+                                    void* o, float* lse, void* ws, size_t ws_bytes, vecattn_stream_t stream) {
+    vecattn_status_t st = check_problem(p);
+    if (st != VECATTN_OK) return st;
+    if ((pq != 64 && pq != 128) || !q || !k || !v || !offsets || !o || nnz_cap < 0 || (nnz_cap > 0 && !indices))
+        return VECATTN_ERR_INVALID_ARGUMENT;
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return VECATTN_ERR_SHAPE;
+    const size_t need = vecattn_sparse_workspace_bytes(p, pq, nnz_cap);
+    if (!ws || ws_bytes < need) return VECATTN_ERR_WORKSPACE;
+    cudaStream_t cs = (cudaStream_t)stream;
+    AttnParams* ap = new AttnParams;
+    st = attn_common(p, q, k, v, o, lse, *ap);
+    const int64_t rows_kv = p->B * p->Hkv * p->N;
+    if (st == VECATTN_OK && (!tmap_gather(&ap->tm_k, k, (uint64_t)p->D, (uint64_t)rows_kv) ||
+                             !tmap_gather(&ap->tm_v, v, (uint64_t)p->D, (uint64_t)rows_kv)))
+        st = VECATTN_ERR_UNSUPPORTED;
+    if (st != VECATTN_OK) { delete ap; return st; }
+    uint8_t* b = static_cast<uint8_t*>(ws);
+    uint32_t* wl = reinterpret_cast<uint32_t*>(b);
+    int32_t* wl_len = reinterpret_cast<int32_t*>(b + align_up((size_t)nnz_cap * 4));
+    int* counter = reinterpret_cast<int*>(b + align_up((size_t)nnz_cap * 4) + align_up((size_t)(ap->BH * ap->n_mt) * 4));
+    ap->Np = n_pooled(p, pq);
+    ap->pq = pq;
+    ap->wl = wl;
+    ap->offsets = offsets;
+    ap->wl_len = wl_len;
+    ap->work_counter = counter;
+    cudaError_t e = va::launch_worklist(offsets, indices ? indices : reinterpret_cast<const int32_t*>(wl), wl, wl_len,
+                                        ap->BH, ap->Np, ap->n_mt, pq, cs);
+    if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, sizeof(int), cs);
+    if (e == cudaSuccess) e = va::launch_attn(*ap, (int)p->D, true, attn_grid(ap->total_items), cs);
+    delete ap;
+    return e == cudaSuccess ? VECATTN_OK : VECATTN_ERR_CUDA;
+}
+
+size_t vecattn_dense_workspace_bytes(const vecattn_problem_t* p) {
+    if (check_problem(p) != VECATTN_OK) return 0;
+    return kAlign;
+}
+
+vecattn_status_t vecattn_dense_fwd(const vecattn_problem_t* p, const void* q, const void* k, const void* v, void* o,
+                                   float* lse, void* ws, size_t ws_bytes, vecattn_stream_t stream) {
+    vecattn_status_t st = check_problem(p);
+    if (st != VECATTN_OK) return st;
+    if (!q || !k || !v || !o) return VECATTN_ERR_INVALID_ARGUMENT;
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return VECATTN_ERR_SHAPE;
+    if (!ws || ws_bytes < kAlign) return VECATTN_ERR_WORKSPACE;
+    cudaStream_t cs = (cudaStream_t)stream;
+    AttnParams* ap = new AttnParams;
+    st = attn_common(p, q, k, v, o, lse, *ap);
+    if (st == VECATTN_OK &&
+        (!tmap_3d(&ap->tm_k, k, (uint64_t)p->D, (uint64_t)p->N, (uint64_t)(p->B * p->Hkv), 128) ||
+         !tmap_3d(&ap->tm_v, v, (uint64_t)p->D, (uint64_t)p->N, (uint64_t)(p->B * p->Hkv), 128)))
+        st = VECATTN_ERR_UNSUPPORTED;
+    if (st != VECATTN_OK) { delete ap; return st; }
+    ap->Np = ap->n_mt;
+    ap->pq = 128;
+    ap->work_counter = reinterpret_cast<int*>(ws);
+    cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(int), cs);
+    if (e == cudaSuccess) e = va::launch_attn(*ap, (int)p->D, false, attn_grid(ap->total_items), cs);
+    delete ap;
+    return e == cudaSuccess ? VECATTN_OK : VECATTN_ERR_CUDA;
+}
+
+vecattn_status_t vecattn_validate_selection(const vecattn_problem_t* p, int32_t pq, const int64_t* offsets,
+                                            const int32_t* indices, int32_t* d_bad, vecattn_stream_t stream) {
+    vecattn_status_t st = check_problem(p);
+    if (st != VECATTN_OK) return st;
+    if ((pq != 64 && pq != 128) || !offsets || !d_bad) return VECATTN_ERR_INVALID_ARGUMENT;
+    cudaStream_t cs = (cudaStream_t)stream;
+    const int64_t Np = n_pooled(p, pq), R = p->B * p->Hq * Np;
+    VA_CU(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), cs));
+    validate_kernel<<<(unsigned)((R + 255) / 256), 256, 0, cs>>>(offsets, indices, R, Np, p->N, pq,
+                                                                  p->causal ? 1 : 0, d_bad);
+    VA_CU(cudaGetLastError());
+    return VECATTN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// kernels.cuh — launch-side interface between the C-ABI host layer (host.cu) and
+// the kernels (pool.cu, select.cu, compact.cu, attn.cu).  Internal to the library.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <cuda_bf16.h>
+
+namespace va {
+
+constexpr int kNumSMsB200 = 148;
+
+// ----------------------------------------------------------------------- pooling
+// Eq. 2: qp[bh,i,:] = bf16_RNE( fp64 sum_{r in block i} q[bh,r,:] / h_i )
+cudaError_t launch_pool(const void* q, void* qp, int64_t BH, int64_t N, int64_t D, int32_t pq,
+                        cudaStream_t st);
+
+// ----------------------------------------------------------------------- selection
+enum SelectEpi : int {
+    EPI_ALG1 = 0,      // Alg. 1: running max per B_K chunk, reset per group of G_K tiles
+    EPI_MAX = 1,       // EXACT pass 1: row max over visible keys -> rowmax (ordered u32)
+    EPI_THRESH = 2,    // EXACT pass 2: keep s >= rowmax - alpha
+    EPI_TOPK_HIST = 3, // TOPK radix pass (8-bit digit `pass`)
+    EPI_TOPK_EMIT = 4, // TOPK: keep key > theta, plus the first k_rem ties in index order
+    EPI_SCORES = 5,    // debug: dump raw fp32 accumulators
+};
+
+struct SelectParams {
+    alignas(64) CUtensorMap tm_qp;  // 3-D {D, Np, B*Hq}, box {64, 128, 1}, SW128
+    alignas(64) CUtensorMap tm_k;   // 3-D {D, N, B*Hkv}, box {64, BN, 1}, SW128
+    int64_t N, Np, BH, Hq, Hkv;
+    int32_t pq, causal, bk, gk;
+    int64_t seg_len;               // keys per CTA unit (multiple of BN and of bk*gk, or >= N)
+    int64_t n_seg;                 // segments per row tile
+    int64_t n_mt;                  // 128-row tiles per head
+    int64_t words_per_row;         // bitmask row stride (u32 words)
+    uint32_t* bitmask;             // [BH*Np, words_per_row]
+    unsigned long long* counts;    // [BH*Np]
+    uint32_t* rowmax;              // [BH*Np] ordered keys (EXACT)
+    uint32_t* tk_prefix;           // [BH*Np] TOPK radix state
+    uint32_t* tk_krem;             // [BH*Np]
+    float* scores_out;             // EPI_SCORES: [BH*Np, N] fp32 (debug)
+    int32_t pass;                  // TOPK pass 0..3
+    int64_t topk;                  // TOPK budget
+    float keep_frac;
+    float alpha_raw[1024];         // per q head: alpha / scale (raw-accumulator units)
+};
+
+cudaError_t launch_select(const SelectParams& p, int epi, int D, cudaStream_t st);
+
+// ---------------------------------------------------------------------- compaction
+// offsets[r+1] = sum counts[0..r]; d_nnz = total.
+cudaError_t launch_scan(const unsigned long long* counts, int64_t R, int64_t* offsets, int64_t* d_nnz,
+                        cudaStream_t st);
+// Emits ascending indices of set bits of each row if *d_nnz <= cap.
+cudaError_t launch_emit(const uint32_t* bitmask, int64_t words_per_row, const int64_t* offsets,
+                        const int64_t* d_nnz, int64_t cap, int32_t* indices, int64_t BH, int64_t Np,
+                        int64_t N, int32_t pq, int32_t causal, cudaStream_t st);
+
+// ----------------------------------------------------------------------- attention
+struct AttnParams {
+    alignas(64) CUtensorMap tm_q;  // 3-D {D, N, B*Hq}, box {64, 128, 1}
+    alignas(64) CUtensorMap tm_k;  // dense: 3-D {D, N, B*Hkv} box {64,128,1}; gather: 2-D {D, B*Hkv*N} box {64,1}
+    alignas(64) CUtensorMap tm_v;
+    const __nv_bfloat16* q;        // raw pointers for the degenerate-row fallback
+    const __nv_bfloat16* k;
+    const __nv_bfloat16* v;
+    __nv_bfloat16* o;              // [B*Hq, N, D]
+    float* lse;                    // [B*Hq, N] or null
+    const uint32_t* wl;            // gather: union entries (key | inA<<30 | inB<<31)
+    const int64_t* offsets;        // gather: CSR offsets [B*Hq*Np + 1] (pair base = offsets[bh*Np + G*pair])
+    const int32_t* wl_len;         // gather: [B*Hq*n_mt] union length per 128-row tile
+    int* work_counter;             // dynamic tile scheduler (zeroed before launch)
+    int64_t N, Np, BH, Hq, Hkv, n_mt, total_items;
+    int32_t pq, causal;
+    float scale, scale_log2;
+};
+
+cudaError_t launch_worklist(const int64_t* offsets, const int32_t* indices, uint32_t* wl, int32_t* wl_len,
+                            int64_t BH, int64_t Np, int64_t n_mt, int32_t pq, cudaStream_t st);
+cudaError_t launch_attn(const AttnParams& p, int D, bool gather, int grid, cudaStream_t st);
+
+}  // namespace va

@@ -1,0 +1,376 @@
+// select.cu — important-vector selection ("TilingSelect" + minS / topK), sm_100a.
+//
+// The pooled-score GEMM S = Q_p K^T (Alg. 1) runs on
+// tcgen05 tensor cores with the 128 x BN score tile held in TMEM; the filter is
+// applied in the epilogue straight out of TMEM, so the estimated attention map is
+// never written to HBM (Sec. 3.1.3).  Only a 1-bit-per-key selection
+// mask leaves the chip; compact.cu turns it into sorted index lists (I, C of
+// Alg. 1).
+//
+// CTA = one work unit (head bh, 128 pooled rows, key segment).  Warp roles:
+//   warp 0  TMA producer: Q_p tile once, then K tiles [BN x D] into a STAGES ring
+//   warp 1  TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16)
+//   warps 2-5 epilogue: thread = pooled row (TMEM lane), 2 TMEM accumulators so the
+//           epilogue of tile t overlaps the MMA of tile t+1.
+// Epilogues (template EPI):
+//   EPI_ALG1   Alg. 1: running row max per B_K chunk, reset every G_K
+//              tiles (reading R2), keep s >= m - alpha AFTER the update
+//              (readings R1 '>=' and R3).
+//   EPI_MAX / EPI_THRESH   Eq. 3: global row max, then fixed threshold.
+//   EPI_TOPK_HIST / EPI_TOPK_EMIT   topK: 4 radix passes over
+//              order-preserving fp32 keys, then emit with ties -> lowest index (R12).
+//   EPI_SCORES debug dump of the raw accumulators (tests only).
+// Comparisons use raw accumulators: s = scale*acc with scale > 0, so
+// s >= m - alpha  <=>  acc >= m_acc - alpha/scale (alpha_raw, computed on host).
+// Causal (reading R5): keys j > L_i = min(N,(i+1)P_q)-1 are excluded before max
+// and filter; keys >= N (ragged tail, R7) likewise.
+#include "common.cuh"
+#include "kernels.cuh"
+
+#include <math.h>
+
+namespace va {
+
+namespace {
+
+constexpr int kThreads = 192;
+
+template <int D, int BN, int STAGES, int EPI>
+struct SelCfg {
+    static constexpr int kCB = D / 64;                       // 128-byte column blocks
+    static constexpr int kQBytes = kCB * 128 * 128;          // Q_p tile
+    static constexpr int kKStageBytes = kCB * BN * 128;      // one K tile
+    static constexpr int kHistBytes = (EPI == EPI_TOPK_HIST) ? 256 * 128 * 4 : 0;
+    static constexpr int kOffQ = 0;
+    static constexpr int kOffK = kQBytes;
+    static constexpr int kOffHist = kOffK + STAGES * kKStageBytes;
+    static constexpr int kOffBar = kOffHist + kHistBytes;
+    static constexpr int kNumBars = 1 + 2 * STAGES + 4;
+    static constexpr int kSmem = kOffBar + kNumBars * 8 + 16;
+    static constexpr uint32_t kTmemCols = 2 * BN;
+    static constexpr uint32_t kIdesc = make_idesc_bf16(128, BN, 0, 0);
+};
+
+VA_DEV float fmax3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
+
+}  // namespace
+
+template <int D, int BN, int STAGES, int EPI, int BK>
+__global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_constant__ SelectParams p) {
+    using C = SelCfg<D, BN, STAGES, EPI>;
+    extern __shared__ __align__(1024) uint8_t smem[];
+
+    // ---- unit decode: unit = ((bh * n_mt) + mt) * n_seg + seg
+    const int64_t unit = blockIdx.x;
+    const int64_t seg = unit % p.n_seg;
+    const int64_t mt = (unit / p.n_seg) % p.n_mt;
+    const int64_t bh = unit / (p.n_seg * p.n_mt);
+    const int64_t m0 = mt * 128;
+    const int64_t row_hi = min(p.Np, m0 + 128);  // exclusive
+    const int64_t kend_tile = p.causal ? min(p.N, row_hi * (int64_t)p.pq) : p.N;
+    const int64_t k_begin = seg * p.seg_len;
+    const int64_t k_end = min(k_begin + p.seg_len, kend_tile);
+    if (k_begin >= k_end) return;  // uniform: causal units above the diagonal
+    const int n_tiles = (int)((k_end - k_begin + BN - 1) / BN);
+    const int64_t b = bh / p.Hq;
+    const int64_t h = bh % p.Hq;
+    const int64_t bh_kv = b * p.Hkv + h / (p.Hq / p.Hkv);
+
+    uint8_t* sQ = smem + C::kOffQ;
+    uint8_t* sK = smem + C::kOffK;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+    uint64_t* q_full = bars;
+    uint64_t* k_full = bars + 1;
+    uint64_t* k_empty = bars + 1 + STAGES;
+    uint64_t* acc_full = bars + 1 + 2 * STAGES;
+    uint64_t* acc_empty = bars + 3 + 2 * STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
+
+    const uint32_t warp = warp_id();
+    const uint32_t lane = lane_id();
+
+    if (threadIdx.x == 0) {
+        if ((smem_u32(smem) & 1023u) != 0) __trap();  // SW128 tiles need 1024-B alignment
+        mbar_init(q_full, 1);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&k_full[s], 1);
+            mbar_init(&k_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&acc_full[s], 1);
+            mbar_init(&acc_empty[s], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ================================================================ producer
+        if (elect_one()) {
+            tma_prefetch_desc(&p.tm_qp);
+            tma_prefetch_desc(&p.tm_k);
+            mbar_arrive_expect_tx(q_full, C::kQBytes);
+#pragma unroll
+            for (int cb = 0; cb < C::kCB; ++cb)
+                tma_load_3d(sQ + cb * 128 * 128, &p.tm_qp, q_full, cb * 64, (int)m0, (int)bh);
+            for (int t = 0; t < n_tiles; ++t) {
+                const int s = t % STAGES;
+                if (t >= STAGES) mbar_wait(&k_empty[s], ((t / STAGES) - 1) & 1);
+                mbar_arrive_expect_tx(&k_full[s], C::kKStageBytes);
+                const int key0 = (int)(k_begin + (int64_t)t * BN);
+#pragma unroll
+                for (int cb = 0; cb < C::kCB; ++cb)
+                    tma_load_3d(sK + s * C::kKStageBytes + cb * BN * 128, &p.tm_k, &k_full[s], cb * 64, key0,
+                                (int)bh_kv);
+            }
+        }
+    } else if (warp == 1) {
+        // ================================================================ MMA issuer
+        if (elect_one()) {
+            mbar_wait(q_full, 0);
+            tc_fence_after();
+            const uint32_t qa = smem_u32(sQ);
+            for (int t = 0; t < n_tiles; ++t) {
+                const int s = t % STAGES;
+                const int buf = t & 1;
+                mbar_wait(&k_full[s], (t / STAGES) & 1);
+                if (t >= 2) mbar_wait(&acc_empty[buf], ((t >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint32_t ka = smem_u32(sK + s * C::kKStageBytes);
+                const uint32_t d_tmem = tmem_base + (uint32_t)(buf * BN);
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const uint64_t adesc = make_sdesc(qa + (kk >> 2) * 128 * 128 + (kk & 3) * 32, 16, 1024);
+                    const uint64_t bdesc = make_sdesc(ka + (kk >> 2) * BN * 128 + (kk & 3) * 32, 16, 1024);
+                    mma_bf16_ss(d_tmem, adesc, bdesc, C::kIdesc, kk > 0 ? 1u : 0u);
+                }
+                mma_commit(&k_empty[s]);
+                mma_commit(&acc_full[buf]);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ================================================================ epilogue
+        const uint32_t quad = warp & 3u;
+        const int r = (int)(quad * 32 + lane);
+        const int64_t i = m0 + r;                  // pooled row within head
+        const bool row_ok = i < p.Np;
+        const int64_t grow = bh * p.Np + i;        // global row id
+        const int64_t vis_end = p.causal ? min(p.N, (i + 1) * (int64_t)p.pq) : p.N;
+        const float alpha_raw = p.alpha_raw[h];
+        const int64_t G = (int64_t)p.bk * (int64_t)p.gk;
+        int64_t next_reset = k_begin;              // Alg. 1 group boundaries (multiples of G)
+        float m_run = -INFINITY;                   // ALG1 running max / EPI_MAX row max
+        float thr_fixed = 0.f;
+        uint32_t tk_prefix = 0, tk_krem = 0, tk_taken = 0;
+        unsigned long long cnt = 0;
+        uint32_t* hist = reinterpret_cast<uint32_t*>(smem + C::kOffHist);
+
+        if constexpr (EPI == EPI_THRESH) {
+            if (row_ok) thr_fixed = f32_from_order_key(p.rowmax[grow]) - alpha_raw;
+        }
+        if constexpr (EPI == EPI_TOPK_HIST || EPI == EPI_TOPK_EMIT) {
+            if (row_ok) {
+                if (EPI == EPI_TOPK_HIST && p.pass == 0) {
+                    int64_t ki;
+                    if (p.topk > 0) ki = min(p.topk, vis_end);
+                    else {
+                        ki = (int64_t)floor((double)p.keep_frac * (double)vis_end + 0.5);
+                        ki = max((int64_t)1, min(ki, vis_end));
+                    }
+                    tk_prefix = 0;
+                    tk_krem = (uint32_t)ki;
+                } else {
+                    tk_prefix = p.tk_prefix[grow];
+                    tk_krem = p.tk_krem[grow];
+                }
+            }
+            if constexpr (EPI == EPI_TOPK_HIST) {
+                for (int bin = 0; bin < 256; ++bin) hist[bin * 128 + r] = 0u;  // own column only
+            }
+        }
+
+        for (int t = 0; t < n_tiles; ++t) {
+            const int buf = t & 1;
+            mbar_wait(&acc_full[buf], (t >> 1) & 1);
+            tc_fence_after();
+            const int64_t key0 = k_begin + (int64_t)t * BN;
+            uint32_t words[BN / 32];
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c) {
+                uint32_t va_[32], vb_[32];
+                const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + (uint32_t)(buf * BN + c * 64);
+                tmem_ld32(taddr, va_);
+                tmem_ld32(taddr + 32, vb_);
+                tmem_ld_wait();
+                float v[64];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    v[j] = __uint_as_float(va_[j]);
+                    v[32 + j] = __uint_as_float(vb_[j]);
+                }
+                const int64_t kc = key0 + c * 64;                 // first key of this 64-chunk
+                const int64_t nv64 = vis_end - kc;                // visible prefix length
+                const int nvis = row_ok ? (int)max((int64_t)0, min((int64_t)64, nv64)) : 0;
+                uint32_t w0 = 0, w1 = 0;
+
+                if constexpr (EPI == EPI_SCORES) {
+                    if (row_ok) {
+#pragma unroll
+                        for (int j = 0; j < 64; ++j)
+                            if (kc + j < p.N) p.scores_out[grow * p.N + kc + j] = v[j];
+                    }
+                } else if constexpr (EPI == EPI_ALG1) {
+                    if (nvis < 64) {
+#pragma unroll
+                        for (int j = 0; j < 64; ++j)
+                            if (j >= nvis) v[j] = -INFINITY;
+                    }
+#pragma unroll
+                    for (int sub = 0; sub < 64; sub += BK) {
+                        if (kc + sub == next_reset) {  // new group of G_K tiles: m_S <- -inf
+                            m_run = -INFINITY;
+                            next_reset += G;
+                        }
+                        float mx = -INFINITY;
+#pragma unroll
+                        for (int j = 0; j < BK; j += 2) mx = fmax3(mx, v[sub + j], v[sub + j + 1]);
+                        m_run = fmaxf(m_run, mx);                 // m_S <- max(m_S, rowmax(S_tile))
+                        const float thr = m_run - alpha_raw;      // M <- S >= m_S - alpha (R1)
+                        if (nvis >= 64) {
+#pragma unroll
+                            for (int j = sub; j < sub + BK; ++j) {
+                                const uint32_t keep = v[j] >= thr ? 1u : 0u;
+                                if (j < 32) w0 |= keep << j;
+                                else w1 |= keep << (j - 32);
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = sub; j < sub + BK; ++j) {
+                                const uint32_t keep = (j < nvis) && (v[j] >= thr) ? 1u : 0u;
+                                if (j < 32) w0 |= keep << j;
+                                else w1 |= keep << (j - 32);
+                            }
+                        }
+                    }
+                } else if constexpr (EPI == EPI_MAX) {
+#pragma unroll
+                    for (int j = 0; j < 64; ++j)
+                        if (j < nvis) m_run = fmaxf(m_run, v[j]);
+                } else if constexpr (EPI == EPI_THRESH) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        w0 |= ((j < nvis) && (v[j] >= thr_fixed) ? 1u : 0u) << j;
+                        w1 |= ((j + 32 < nvis) && (v[j + 32] >= thr_fixed) ? 1u : 0u) << j;
+                    }
+                } else if constexpr (EPI == EPI_TOPK_HIST) {
+                    const int pass = p.pass;
+#pragma unroll
+                    for (int j = 0; j < 64; ++j) {
+                        if (j >= nvis) break;
+                        const uint32_t u = f32_order_key(v[j]);
+                        const bool match = (pass == 0) || ((u >> (32 - 8 * pass)) == tk_prefix);
+                        if (match) hist[((u >> (24 - 8 * pass)) & 255u) * 128 + r] += 1u;
+                    }
+                } else if constexpr (EPI == EPI_TOPK_EMIT) {
+#pragma unroll
+                    for (int j = 0; j < 64; ++j) {
+                        if (j >= nvis) break;
+                        const uint32_t u = f32_order_key(v[j]);
+                        bool keep = u > tk_prefix;
+                        if (u == tk_prefix && tk_taken < tk_krem) {
+                            keep = true;
+                            ++tk_taken;
+                        }
+                        if (j < 32) w0 |= (keep ? 1u : 0u) << j;
+                        else w1 |= (keep ? 1u : 0u) << (j - 32);
+                    }
+                }
+                words[2 * c] = w0;
+                words[2 * c + 1] = w1;
+            }
+            tc_fence_before();
+            mbar_arrive(&acc_empty[buf]);
+
+            if constexpr (EPI == EPI_ALG1 || EPI == EPI_THRESH || EPI == EPI_TOPK_EMIT) {
+                if (row_ok) {
+                    uint32_t* dst = p.bitmask + grow * p.words_per_row + key0 / 32;
+#pragma unroll
+                    for (int w = 0; w < BN / 32; w += 4) {
+                        *reinterpret_cast<uint4*>(dst + w) = make_uint4(words[w], words[w + 1], words[w + 2], words[w + 3]);
+                        cnt += __popc(words[w]) + __popc(words[w + 1]) + __popc(words[w + 2]) + __popc(words[w + 3]);
+                    }
+                }
+            }
+        }
+
+        if (row_ok) {
+            if constexpr (EPI == EPI_ALG1 || EPI == EPI_THRESH || EPI == EPI_TOPK_EMIT) {
+                if (cnt) atomicAdd(&p.counts[grow], cnt);
+            } else if constexpr (EPI == EPI_MAX) {
+                if (m_run > -INFINITY) atomicMax(&p.rowmax[grow], f32_order_key(m_run));
+            } else if constexpr (EPI == EPI_TOPK_HIST) {
+                // find the bin holding the krem-th largest remaining key (scan from the top)
+                uint32_t cum = 0;
+                int bin = 255;
+                for (; bin > 0; --bin) {
+                    const uint32_t hc = hist[bin * 128 + r];
+                    if (cum + hc >= tk_krem) break;
+                    cum += hc;
+                }
+                p.tk_prefix[grow] = (tk_prefix << 8) | (uint32_t)bin;
+                p.tk_krem[grow] = tk_krem - cum;
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<C::kTmemCols>(tmem_base);
+    }
+}
+
+template <int D, int BN, int STAGES, int EPI, int BK = 16>
+static cudaError_t launch_sel_t(const SelectParams& p, cudaStream_t st) {
+    using C = SelCfg<D, BN, STAGES, EPI>;
+    auto kern = select_kernel<D, BN, STAGES, EPI, BK>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if (e != cudaSuccess) return e;
+    const int64_t units = p.BH * p.n_mt * p.n_seg;
+    if (units <= 0) return cudaSuccess;
+    kern<<<(unsigned)units, kThreads, C::kSmem, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t launch_sel_d(const SelectParams& p, int epi, cudaStream_t st) {
+    switch (epi) {
+        case EPI_ALG1:
+            if (p.bk == 16) return launch_sel_t<D, 256, 3, EPI_ALG1, 16>(p, st);
+            if (p.bk == 32) return launch_sel_t<D, 256, 3, EPI_ALG1, 32>(p, st);
+            if (p.bk == 64) return launch_sel_t<D, 256, 3, EPI_ALG1, 64>(p, st);
+            return cudaErrorInvalidValue;
+        case EPI_MAX: return launch_sel_t<D, 256, 3, EPI_MAX>(p, st);
+        case EPI_THRESH: return launch_sel_t<D, 256, 3, EPI_THRESH>(p, st);
+        case EPI_TOPK_HIST: return launch_sel_t<D, 128, 2, EPI_TOPK_HIST>(p, st);
+        case EPI_TOPK_EMIT: return launch_sel_t<D, 256, 3, EPI_TOPK_EMIT>(p, st);
+        case EPI_SCORES: return launch_sel_t<D, 256, 3, EPI_SCORES>(p, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+int select_bn(int epi) { return epi == EPI_TOPK_HIST ? 128 : 256; }
+
+cudaError_t launch_select(const SelectParams& p, int epi, int D, cudaStream_t st) {
+    if (D == 128) return launch_sel_d<128>(p, epi, st);
+    if (D == 64) return launch_sel_d<64>(p, epi, st);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace va

@@ -1,0 +1,271 @@
+"""Thin ctypes binding of include/vecattn.h (argument marshalling only).
+
+Every step of the hot path runs in libvecattn.so's sm_100a kernels; torch is
+used for device memory and streams.  There is no CPU or eager fallback: if the
+library is missing or the device is not sm_100, these functions raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvecattn.so")
+
+SEL_MINS_ALG1 = 0
+SEL_MINS_EXACT = 1
+SEL_TOPK = 2
+MODES = {"alg1": SEL_MINS_ALG1, "exact": SEL_MINS_EXACT, "topk": SEL_TOPK}
+
+STATUS = {0: "ok", 1: "invalid argument", 2: "shape", 3: "unsupported", 4: "workspace", 5: "cuda"}
+
+
+class VecAttnError(RuntimeError):
+    def __init__(self, fn, code):
+        super().__init__(f"{fn} failed: {STATUS.get(code, code)} ({code})")
+        self.code = code
+
+
+class Problem(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int64), ("Hq", ctypes.c_int64), ("Hkv", ctypes.c_int64), ("N", ctypes.c_int64),
+                ("D", ctypes.c_int64), ("causal", ctypes.c_int32), ("scale", ctypes.c_float)]
+
+
+class SelectParams(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("pq", ctypes.c_int32), ("bk", ctypes.c_int32), ("gk", ctypes.c_int32),
+                ("alpha", ctypes.c_float), ("alpha_per_head", ctypes.POINTER(ctypes.c_float)),
+                ("topk", ctypes.c_int64), ("keep_frac", ctypes.c_float)]
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load libvecattn.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not found: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    P, vp = ctypes.POINTER, ctypes.c_void_p
+    i32, i64, sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    prob, sel = P(Problem), P(SelectParams)
+    sig = {
+        "vecattn_pool": (i32, [prob, i32, vp, vp, vp]),
+        "vecattn_select_workspace_bytes": (sz, [prob, sel]),
+        "vecattn_select": (i32, [prob, sel, vp, vp, vp, vp, i64, vp, vp, sz, vp]),
+        "vecattn_sparse_workspace_bytes": (sz, [prob, i32, i64]),
+        "vecattn_sparse_fwd": (i32, [prob, i32, vp, vp, vp, vp, vp, i64, vp, vp, vp, sz, vp]),
+        "vecattn_dense_workspace_bytes": (sz, [prob]),
+        "vecattn_dense_fwd": (i32, [prob, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "vecattn_validate_selection": (i32, [prob, i32, vp, vp, vp, vp]),
+        "vecattn_debug_scores": (i32, [prob, i32, vp, vp, vp, vp, sz, vp]),
+        "vecattn_status_string": (ctypes.c_char_p, [i32]),
+        "vecattn_abi_version": (i32, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+EXPORTED = ["vecattn_pool", "vecattn_select_workspace_bytes", "vecattn_select", "vecattn_sparse_workspace_bytes",
+            "vecattn_sparse_fwd", "vecattn_dense_workspace_bytes", "vecattn_dense_fwd",
+            "vecattn_validate_selection", "vecattn_debug_scores", "vecattn_status_string", "vecattn_abi_version"]
+
+
+def _ptr(t):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check(fn, rc):
+    if rc != 0:
+        raise VecAttnError(fn, rc)
+
+
+def _dev_check(*ts):
+    for t in ts:
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise ValueError("vecattn: tensors must be CUDA device tensors (no CPU fallback)")
+        if not t.is_contiguous():
+            raise ValueError("vecattn: tensors must be contiguous")
+
+
+def problem(q: torch.Tensor, k: torch.Tensor, causal: bool, scale: float | None = None) -> Problem:
+    B, Hq, N, D = q.shape
+    Hkv = k.shape[1]
+    return Problem(B, Hq, Hkv, N, D, int(bool(causal)), 0.0 if scale is None else float(scale))
+
+
+@dataclass
+class SelectConfig:
+    mode: str = "alg1"
+    pq: int = 64
+    bk: int = 16
+    gk: int = 16
+    alpha: float = 0.0
+    alpha_per_head: list | None = None
+    topk: int = 0
+    keep_frac: float = 0.0
+
+    def params(self) -> SelectParams:
+        sp = SelectParams()
+        sp.mode, sp.pq, sp.bk, sp.gk = MODES[self.mode], self.pq, self.bk, self.gk
+        sp.alpha = float(self.alpha)
+        if self.alpha_per_head is not None:
+            arr = (ctypes.c_float * len(self.alpha_per_head))(*[float(a) for a in self.alpha_per_head])
+            sp.alpha_per_head = ctypes.cast(arr, ctypes.POINTER(ctypes.c_float))
+            sp._keep = arr  # keep alive
+        sp.topk = int(self.topk)
+        sp.keep_frac = float(self.keep_frac)
+        return sp
+
+
+class Workspace:
+    """Caller-owned device workspace, grown on demand (allocation happens outside the hot loop)."""
+
+    def __init__(self, device="cuda"):
+        self.device = device
+        self.buf = None
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        nbytes = max(int(nbytes), 256)
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
+def pool(q: torch.Tensor, pq: int = 64, stream=None) -> torch.Tensor:
+    lib = load()
+    _dev_check(q)
+    B, H, N, D = q.shape
+    Np = (N + pq - 1) // pq
+    qp = torch.empty(B, H, Np, D, dtype=torch.bfloat16, device=q.device)
+    pr = problem(q, q, False)
+    _check("vecattn_pool", lib.vecattn_pool(ctypes.byref(pr), pq, _ptr(q), _ptr(qp), _stream(stream)))
+    return qp
+
+
+def select_workspace_bytes(pr: Problem, cfg: SelectConfig) -> int:
+    return int(load().vecattn_select_workspace_bytes(ctypes.byref(pr), ctypes.byref(cfg.params())))
+
+
+def select_into(q, k, cfg: SelectConfig, offsets, indices, cap: int, d_nnz, ws: torch.Tensor, causal: bool,
+                scale=None, stream=None):
+    """Raw vecattn_select call into caller buffers (no host sync)."""
+    lib = load()
+    _dev_check(q, k, offsets, indices, d_nnz)
+    pr = problem(q, k, causal, scale)
+    sp = cfg.params()
+    rc = lib.vecattn_select(ctypes.byref(pr), ctypes.byref(sp), _ptr(q), _ptr(k), _ptr(offsets), _ptr(indices),
+                            int(cap), _ptr(d_nnz), _ptr(ws), ws.numel(), _stream(stream))
+    _check("vecattn_select", rc)
+
+
+def select(q, k, cfg: SelectConfig, causal: bool = False, scale=None, ws: Workspace | None = None,
+           cap: int | None = None, stream=None):
+    """Selection with the capacity protocol: returns (offsets int64, indices int32)."""
+    B, H, N, D = q.shape
+    Np = (N + cfg.pq - 1) // cfg.pq
+    pr = problem(q, k, causal, scale)
+    ws = ws or Workspace(q.device)
+    wbuf = ws.get(select_workspace_bytes(pr, cfg))
+    offsets = torch.empty(B * H * Np + 1, dtype=torch.int64, device=q.device)
+    d_nnz = torch.empty(1, dtype=torch.int64, device=q.device)
+    if cap is None:
+        select_into(q, k, cfg, offsets, None, 0, d_nnz, wbuf, causal, scale, stream)
+        cap = int(d_nnz.item())
+    indices = torch.empty(max(cap, 1), dtype=torch.int32, device=q.device)
+    select_into(q, k, cfg, offsets, indices, max(cap, 1), d_nnz, wbuf, causal, scale, stream)
+    nnz = int(d_nnz.item())
+    if nnz > cap:
+        return select(q, k, cfg, causal, scale, ws, nnz, stream)
+    return offsets, indices[:nnz]
+
+
+def debug_scores(q, k, pq: int = 64, ws: Workspace | None = None, stream=None) -> torch.Tensor:
+    lib = load()
+    _dev_check(q, k)
+    B, H, N, D = q.shape
+    Np = (N + pq - 1) // pq
+    pr = problem(q, k, False)
+    cfg = SelectConfig(pq=pq)
+    ws = ws or Workspace(q.device)
+    wbuf = ws.get(select_workspace_bytes(pr, cfg))
+    out = torch.full((B * H * Np, N), float("nan"), dtype=torch.float32, device=q.device)
+    _check("vecattn_debug_scores", lib.vecattn_debug_scores(ctypes.byref(pr), pq, _ptr(q), _ptr(k), _ptr(out),
+                                                              _ptr(wbuf), wbuf.numel(), _stream(stream)))
+    return out
+
+
+def sparse_workspace_bytes(pr: Problem, pq: int, nnz_cap: int) -> int:
+    return int(load().vecattn_sparse_workspace_bytes(ctypes.byref(pr), pq, int(nnz_cap)))
+
+
+def sparse_fwd_into(q, k, v, offsets, indices, pq, o, lse, ws: torch.Tensor, nnz_cap: int, causal: bool,
+                    scale=None, stream=None):
+    lib = load()
+    _dev_check(q, k, v, offsets, indices, o, lse)
+    pr = problem(q, k, causal, scale)
+    rc = lib.vecattn_sparse_fwd(ctypes.byref(pr), pq, _ptr(q), _ptr(k), _ptr(v), _ptr(offsets), _ptr(indices),
+                                int(nnz_cap), _ptr(o), _ptr(lse), _ptr(ws), ws.numel(), _stream(stream))
+    _check("vecattn_sparse_fwd", rc)
+
+
+def sparse_fwd(q, k, v, offsets, indices, pq: int = 64, causal: bool = False, scale=None,
+               ws: Workspace | None = None, with_lse: bool = True, stream=None):
+    B, H, N, D = q.shape
+    pr = problem(q, k, causal, scale)
+    nnz_cap = max(int(indices.numel()), 1)
+    ws = ws or Workspace(q.device)
+    wbuf = ws.get(sparse_workspace_bytes(pr, pq, nnz_cap))
+    o = torch.empty_like(q)
+    lse = torch.empty(B, H, N, dtype=torch.float32, device=q.device) if with_lse else None
+    sparse_fwd_into(q, k, v, offsets, indices, pq, o, lse, wbuf, nnz_cap, causal, scale, stream)
+    return o, lse
+
+
+def dense_fwd_into(q, k, v, o, lse, ws: torch.Tensor, causal: bool, scale=None, stream=None):
+    lib = load()
+    _dev_check(q, k, v, o, lse)
+    pr = problem(q, k, causal, scale)
+    rc = lib.vecattn_dense_fwd(ctypes.byref(pr), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(ws),
+                               ws.numel(), _stream(stream))
+    _check("vecattn_dense_fwd", rc)
+
+
+def dense_fwd(q, k, v, causal: bool = False, scale=None, with_lse: bool = True, stream=None):
+    B, H, N, D = q.shape
+    o = torch.empty_like(q)
+    lse = torch.empty(B, H, N, dtype=torch.float32, device=q.device) if with_lse else None
+    ws = torch.empty(256, dtype=torch.uint8, device=q.device)
+    dense_fwd_into(q, k, v, o, lse, ws, causal, scale, stream)
+    return o, lse
+
+
+def validate_selection(offsets, indices, q_shape, pq: int, causal: bool, stream=None) -> int:
+    lib = load()
+    B, H, N, D = q_shape
+    pr = Problem(B, H, H, N, D, int(causal), 0.0)
+    bad = torch.zeros(1, dtype=torch.int32, device=offsets.device)
+    _check("vecattn_validate_selection", lib.vecattn_validate_selection(
+        ctypes.byref(pr), pq, _ptr(offsets), _ptr(indices), _ptr(bad), _stream(stream)))
+    return int(bad.item())
+
+
+def default_scale(D: int) -> float:
+    return 1.0 / math.sqrt(D)
