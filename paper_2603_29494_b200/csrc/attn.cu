@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
                 tc_fence_after();
                 const uint32_t st = tmem_base + lane_off + (uint32_t)((c & 1) * 128);
                 uint32_t sr[4][32];
+                __syncwarp();  // reconverge after the per-row causal search (tcgen05.ld is .sync.aligned)
 #pragma unroll
                 for (int g = 0; g < 4; ++g) tmem_ld32(st + g * 32, sr[g]);
                 tmem_ld_wait();
@@ -368,22 +369,26 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
                     mbar_wait(&bars[C::B_ODONE], (uint32_t)((c - 1) & 1));
                     tc_fence_after();
                 }
-                if (m_new > m_ref + 8.0f) {
-                    const float corr = ex2(m_ref - m_new);
-                    if (j > 0) {
-#pragma unroll
-                        for (int g = 0; g < D / 32; ++g) {
-                            uint32_t o[32];
-                            tmem_ld32(tmem_O + lane_off + g * 32, o);
-                            tmem_ld_wait();
-#pragma unroll
-                            for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * corr);
-                            tmem_st32(tmem_O + lane_off + g * 32, o);
-                        }
-                        tmem_st_wait();
-                    }
+                // Lazy rescale (only when the max grew by > 2^8): per-row decision, but
+                // tcgen05.ld/st are warp-collective (.sync.aligned), so the O update is
+                // done by the whole warp whenever any lane needs it (others scale by 1).
+                const bool need = m_new > m_ref + 8.0f;
+                const float corr = need ? ex2(m_ref - m_new) : 1.0f;
+                if (need) {
                     l *= corr;
                     m_ref = m_new;
+                }
+                if (j > 0 && __any_sync(0xffffffffu, need)) {
+#pragma unroll
+                    for (int g = 0; g < D / 32; ++g) {
+                        uint32_t o[32];
+                        tmem_ld32(tmem_O + lane_off + g * 32, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * corr);
+                        tmem_st32(tmem_O + lane_off + g * 32, o);
+                    }
+                    tmem_st_wait();
                 }
                 const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
                 uint32_t pk[2][32];
@@ -405,6 +410,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
             // ---------------------------------------------------------------- epilogue
             float o[D];
             if (I.n_chunks > 0) {
+                __syncwarp();
                 mbar_wait(&bars[C::B_ODONE], (uint32_t)((c - 1) & 1));
                 tc_fence_after();
 #pragma unroll
