@@ -32,7 +32,8 @@ namespace va {
 
 namespace {
 
-constexpr int kAttnThreads = 192;
+constexpr int kAttnThreads = 320;   // w0 sched+Q, w1 MMA, w2-5 softmax, w6-9 K/V loaders
+constexpr int kLoadWarps = 4;
 constexpr int kStages = 3;
 constexpr uint32_t kPad = 0x3FFFFFFFu;   // meta key for padding lanes (sorts last)
 
@@ -107,17 +108,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
         mbar_init(&bars[C::B_QFULL], 1);
         mbar_init(&bars[C::B_QEMPTY], 1);
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&bars[C::B_KFULL + s], 1);
+            mbar_init(&bars[C::B_KFULL + s], GATHER ? kLoadWarps : 1);
             mbar_init(&bars[C::B_KEMPTY + s], 1);
-            mbar_init(&bars[C::B_VFULL + s], 1);
+            mbar_init(&bars[C::B_VFULL + s], GATHER ? kLoadWarps : 1);
             mbar_init(&bars[C::B_VEMPTY + s], 1);
-            mbar_init(&bars[C::B_MFULL + s], 1);
+            mbar_init(&bars[C::B_MFULL + s], kLoadWarps);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&bars[C::B_SFULL + s], 1);
             mbar_init(&bars[C::B_PFULL + s], 128);
             mbar_init(&bars[C::B_IFULL + s], 1);
-            mbar_init(&bars[C::B_IEMPTY + s], 1 + 128);
+            mbar_init(&bars[C::B_IEMPTY + s], 1 + 128 + kLoadWarps);
         }
         mbar_init(&bars[C::B_ODONE], 1);
         mbar_init(&bars[C::B_OEMPTY], 128);
@@ -131,14 +132,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
     const uint32_t tmem_O = tmem_base + 256;
 
     if (warp == 0) {
-        // ==================================================================== producer
+        // ============================================ scheduler: dynamic items + Q tile loads
         if (lane == 0) {
             tma_prefetch_desc(&p.tm_q);
             tma_prefetch_desc(&p.tm_k);
             tma_prefetch_desc(&p.tm_v);
         }
-        int64_t c = 0;  // global chunk counter
-        int qi = 0;     // Q loads issued
+        int qi = 0;  // Q loads issued
         for (int it = 0;; ++it) {
             const int slot = it & 1;
             int item = 0;
@@ -152,8 +152,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
             if (item >= p.total_items) break;
             const Item I = decode_item<GATHER>(p, item);
             if (I.n_chunks == 0) continue;
-            const int64_t b = I.bh / p.Hq, h = I.bh % p.Hq;
-            const int64_t bh_kv = b * p.Hkv + h / (p.Hq / p.Hkv);
             if (lane == 0) {
                 if (qi > 0) mbar_wait(&bars[C::B_QEMPTY], (qi - 1) & 1);
                 mbar_arrive_expect_tx(&bars[C::B_QFULL], C::kTileBytes);
@@ -163,71 +161,98 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
                                 (int)I.bh);
             }
             ++qi;
-            for (int j = 0; j < I.n_chunks; ++j, ++c) {
-                const int s = (int)(c % kStages);
-                const int round = (int)(c / kStages);
-                if (lane == 0 && round > 0) {
-                    mbar_wait(&bars[C::B_KEMPTY + s], (round - 1) & 1);
-                    mbar_wait(&bars[C::B_VEMPTY + s], (round - 1) & 1);
-                }
-                __syncwarp();
-                uint8_t* dK = sK + s * C::kTileBytes;
-                uint8_t* dV = sV + s * C::kTileBytes;
-                if constexpr (GATHER) {
-                    // lane owns union entries 4*lane .. 4*lane+3 of this chunk
-                    uint32_t e[4];
-                    int rows[4];
-                    uint32_t nibA = 0, nibB = 0;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int pos = j * 128 + 4 * (int)lane + q;
-                        const bool ok = pos < I.len;
-                        e[q] = ok ? __ldg(p.wl + I.base + pos) : 0u;
-                        const uint32_t key = e[q] & 0x3FFFFFFFu;
-                        rows[q] = (int)(bh_kv * p.N + (ok ? key : 0u));
-                        sMeta[s * C::kMetaWords + 4 * lane + q] = ok ? key : kPad;
-                        nibA |= ((e[q] >> 30) & 1u) << q;
-                        nibB |= ((e[q] >> 31) & 1u) << q;
+        }
+    } else if (warp >= 6) {
+        // ============================================ K/V loaders (4 warps)
+        // GATHER: warp g owns chunk columns [32g, 32g+32): reads its 32 union entries
+        // (prefetched one chunk ahead), publishes keys + membership ballots (mask word g)
+        // to the meta ring, and issues 8 K + 8 V tile::gather4 per column block.
+        // Dense: warp 6 issues the K/V tile loads.
+        const int g = (int)warp - 6;
+        int64_t c = 0;
+        for (int it = 0;; ++it) {
+            const int slot = it & 1;
+            mbar_wait(&bars[C::B_IFULL + slot], (it >> 1) & 1);
+            const int item = item_slot[slot];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars[C::B_IEMPTY + slot]);
+            if (item < 0) break;
+            const Item I = decode_item<GATHER>(p, item);
+            if (I.n_chunks == 0) continue;
+            const int64_t b = I.bh / p.Hq, h = I.bh % p.Hq;
+            const int64_t bh_kv = b * p.Hkv + h / (p.Hq / p.Hkv);
+            if constexpr (GATHER) {
+                const uint32_t* wlp = p.wl + I.base;
+                int pos = 32 * g + (int)lane;
+                uint32_t e_cur = pos < I.len ? __ldg(wlp + pos) : 0u;
+                for (int j = 0; j < I.n_chunks; ++j, ++c) {
+                    const int s = (int)(c % kStages);
+                    const int round = (int)(c / kStages);
+                    const bool ok = pos < I.len;
+                    const int pos_n = pos + 128;
+                    const uint32_t e_nxt = (j + 1 < I.n_chunks && pos_n < I.len) ? __ldg(wlp + pos_n) : 0u;
+                    const uint32_t key = e_cur & 0x3FFFFFFFu;
+                    const int row = (int)(bh_kv * p.N + (ok ? key : 0u));
+                    const uint32_t wA = __ballot_sync(0xffffffffu, ok && ((e_cur >> 30) & 1u));
+                    const uint32_t wB = __ballot_sync(0xffffffffu, ok && ((e_cur >> 31) & 1u));
+                    if (lane == 0 && round > 0) {
+                        mbar_wait(&bars[C::B_KEMPTY + s], (round - 1) & 1);
+                        mbar_wait(&bars[C::B_VEMPTY + s], (round - 1) & 1);
                     }
-                    const uint32_t sh = 4u * (lane & 7u);
-#pragma unroll
-                    for (int wd = 0; wd < 4; ++wd) {
-                        const uint32_t mA = __reduce_or_sync(0xffffffffu, (lane >> 3) == (uint32_t)wd ? nibA << sh : 0u);
-                        const uint32_t mB = __reduce_or_sync(0xffffffffu, (lane >> 3) == (uint32_t)wd ? nibB << sh : 0u);
-                        if (lane == 0) {
-                            sMeta[s * C::kMetaWords + 128 + wd] = mA;
-                            sMeta[s * C::kMetaWords + 132 + wd] = mB;
-                        }
+                    __syncwarp();
+                    uint32_t* meta = sMeta + s * C::kMetaWords;
+                    meta[32 * g + lane] = ok ? key : kPad;
+                    if (lane == 0) {
+                        meta[128 + g] = wA;
+                        meta[132 + g] = wB;
                     }
                     __syncwarp();
                     if (lane == 0) {
                         mbar_arrive(&bars[C::B_MFULL + s]);
-                        mbar_arrive_expect_tx(&bars[C::B_KFULL + s], C::kTileBytes);
-                        mbar_arrive_expect_tx(&bars[C::B_VFULL + s], C::kTileBytes);
+                        mbar_arrive_expect_tx(&bars[C::B_KFULL + s], 32 * D * 2);
+                        mbar_arrive_expect_tx(&bars[C::B_VFULL + s], 32 * D * 2);
                     }
+                    const int r0 = __shfl_sync(0xffffffffu, row, (4 * lane) & 31);
+                    const int r1 = __shfl_sync(0xffffffffu, row, (4 * lane + 1) & 31);
+                    const int r2 = __shfl_sync(0xffffffffu, row, (4 * lane + 2) & 31);
+                    const int r3 = __shfl_sync(0xffffffffu, row, (4 * lane + 3) & 31);
                     __syncwarp();
-#pragma unroll
-                    for (int cb = 0; cb < C::kCB; ++cb)
-                        tma_gather4(dK + cb * 128 * 128 + lane * 4 * 128, &p.tm_k, &bars[C::B_KFULL + s], cb * 64,
-                                    rows[0], rows[1], rows[2], rows[3]);
-#pragma unroll
-                    for (int cb = 0; cb < C::kCB; ++cb)
-                        tma_gather4(dV + cb * 128 * 128 + lane * 4 * 128, &p.tm_v, &bars[C::B_VFULL + s], cb * 64,
-                                    rows[0], rows[1], rows[2], rows[3]);
-                } else {
-                    if (lane == 0) {
-                        mbar_arrive_expect_tx(&bars[C::B_KFULL + s], C::kTileBytes);
+                    if (lane < 8) {
+                        uint8_t* dK = sK + s * C::kTileBytes + (32 * g + 4 * lane) * 128;
+                        uint8_t* dV = sV + s * C::kTileBytes + (32 * g + 4 * lane) * 128;
 #pragma unroll
                         for (int cb = 0; cb < C::kCB; ++cb)
-                            tma_load_3d(dK + cb * 128 * 128, &p.tm_k, &bars[C::B_KFULL + s], cb * 64, j * 128,
-                                        (int)bh_kv);
-                        mbar_arrive_expect_tx(&bars[C::B_VFULL + s], C::kTileBytes);
+                            tma_gather4(dK + cb * 128 * 128, &p.tm_k, &bars[C::B_KFULL + s], cb * 64, r0, r1, r2, r3);
 #pragma unroll
                         for (int cb = 0; cb < C::kCB; ++cb)
-                            tma_load_3d(dV + cb * 128 * 128, &p.tm_v, &bars[C::B_VFULL + s], cb * 64, j * 128,
-                                        (int)bh_kv);
+                            tma_gather4(dV + cb * 128 * 128, &p.tm_v, &bars[C::B_VFULL + s], cb * 64, r0, r1, r2, r3);
                     }
+                    e_cur = e_nxt;
+                    pos = pos_n;
                 }
+            } else {
+                for (int j = 0; j < I.n_chunks; ++j, ++c) {
+                    if (g != 0 || lane != 0) continue;
+                    const int s = (int)(c % kStages);
+                    const int round = (int)(c / kStages);
+                    if (round > 0) {
+                        mbar_wait(&bars[C::B_KEMPTY + s], (round - 1) & 1);
+                        mbar_wait(&bars[C::B_VEMPTY + s], (round - 1) & 1);
+                    }
+                    uint8_t* dK = sK + s * C::kTileBytes;
+                    uint8_t* dV = sV + s * C::kTileBytes;
+                    mbar_arrive_expect_tx(&bars[C::B_KFULL + s], C::kTileBytes);
+#pragma unroll
+                    for (int cb = 0; cb < C::kCB; ++cb)
+                        tma_load_3d(dK + cb * 128 * 128, &p.tm_k, &bars[C::B_KFULL + s], cb * 64, j * 128,
+                                    (int)bh_kv);
+                    mbar_arrive_expect_tx(&bars[C::B_VFULL + s], C::kTileBytes);
+#pragma unroll
+                    for (int cb = 0; cb < C::kCB; ++cb)
+                        tma_load_3d(dV + cb * 128 * 128, &p.tm_v, &bars[C::B_VFULL + s], cb * 64, j * 128,
+                                    (int)bh_kv);
+                }
+                __syncwarp();
             }
         }
     } else if (warp == 1) {
@@ -343,27 +368,32 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
                 mbar_wait(&bars[C::B_SFULL + (c & 1)], (uint32_t)((c >> 1) & 1));
                 tc_fence_after();
                 const uint32_t st = tmem_base + lane_off + (uint32_t)((c & 1) * 128);
-                uint32_t sr[4][32];
-                __syncwarp();  // reconverge after the per-row causal search (tcgen05.ld is .sync.aligned)
-#pragma unroll
-                for (int g = 0; g < 4; ++g) tmem_ld32(st + g * 32, sr[g]);
-                tmem_ld_wait();
-                float sv[128];
-#pragma unroll
-                for (int g = 0; g < 4; ++g)
-#pragma unroll
-                    for (int t = 0; t < 32; ++t) sv[g * 32 + t] = __uint_as_float(sr[g][t]);
                 const bool full = (mw[0] & mw[1] & mw[2] & mw[3]) == 0xffffffffu;
-                if (!full) {
-#pragma unroll
-                    for (int g = 0; g < 4; ++g)
-#pragma unroll
-                        for (int t = 0; t < 32; ++t)
-                            if (!((mw[g] >> t) & 1u)) sv[g * 32 + t] = -INFINITY;
-                }
+                __syncwarp();  // reconverge after the per-row causal search (tcgen05.ld is .sync.aligned)
+                // ---- pass 1: masked row max, 64 TMEM columns at a time (low register pressure)
                 float mx = -INFINITY;
 #pragma unroll
-                for (int t = 0; t < 128; t += 2) mx = fmaxf(fmaxf(mx, sv[t]), sv[t + 1]);
+                for (int hf = 0; hf < 2; ++hf) {
+                    uint32_t a[32], b[32];
+                    tmem_ld32(st + hf * 64, a);
+                    tmem_ld32(st + hf * 64 + 32, b);
+                    tmem_ld_wait();
+                    if (full) {
+#pragma unroll
+                        for (int t = 0; t < 32; t += 2) {
+                            mx = fmaxf(fmaxf(mx, __uint_as_float(a[t])), __uint_as_float(a[t + 1]));
+                            mx = fmaxf(fmaxf(mx, __uint_as_float(b[t])), __uint_as_float(b[t + 1]));
+                        }
+                    } else {
+                        const uint32_t ma = mw[2 * hf], mb = mw[2 * hf + 1];
+#pragma unroll
+                        for (int t = 0; t < 32; ++t) {
+                            const float va_ = (ma & (1u << t)) ? __uint_as_float(a[t]) : -INFINITY;
+                            const float vb_ = (mb & (1u << t)) ? __uint_as_float(b[t]) : -INFINITY;
+                            mx = fmaxf(fmaxf(mx, va_), vb_);
+                        }
+                    }
+                }
                 const float m_new = fmaxf(m_ref, mx * sl2);
                 if (j > 0) {  // O must be stable (previous PV done) before a rescale
                     mbar_wait(&bars[C::B_ODONE], (uint32_t)((c - 1) & 1));
@@ -390,54 +420,72 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
                     }
                     tmem_st_wait();
                 }
+                // ---- pass 2: P = exp2(s*scale*log2e - m), bf16-packed into TMEM over S.
+                // Half hf reads S columns [64hf, 64hf+64) and writes P columns [32hf, 32hf+32),
+                // which only cover S columns already consumed.
                 const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
-                uint32_t pk[2][32];
                 float lsum = 0.f;
 #pragma unroll
-                for (int t = 0; t < 128; t += 2) {
-                    const float p0 = ex2(fmaf(sv[t], sl2, neg_m));
-                    const float p1 = ex2(fmaf(sv[t + 1], sl2, neg_m));
-                    lsum += p0 + p1;
-                    pk[t >> 6][(t >> 1) & 31] = pack_bf16x2(p0, p1);
+                for (int hf = 0; hf < 2; ++hf) {
+                    uint32_t a[32], b[32], pk[32];
+                    tmem_ld32(st + hf * 64, a);
+                    tmem_ld32(st + hf * 64 + 32, b);
+                    tmem_ld_wait();
+                    const uint32_t ma = full ? 0xffffffffu : mw[2 * hf];
+                    const uint32_t mb = full ? 0xffffffffu : mw[2 * hf + 1];
+#pragma unroll
+                    for (int t = 0; t < 32; t += 2) {
+                        float p0 = ex2(fmaf(__uint_as_float(a[t]), sl2, neg_m));
+                        float p1 = ex2(fmaf(__uint_as_float(a[t + 1]), sl2, neg_m));
+                        float p2 = ex2(fmaf(__uint_as_float(b[t]), sl2, neg_m));
+                        float p3 = ex2(fmaf(__uint_as_float(b[t + 1]), sl2, neg_m));
+                        p0 = (ma & (1u << t)) ? p0 : 0.f;
+                        p1 = (ma & (2u << t)) ? p1 : 0.f;
+                        p2 = (mb & (1u << t)) ? p2 : 0.f;
+                        p3 = (mb & (2u << t)) ? p3 : 0.f;
+                        lsum += (p0 + p1) + (p2 + p3);
+                        pk[t >> 1] = pack_bf16x2(p0, p1);
+                        pk[16 + (t >> 1)] = pack_bf16x2(p2, p3);
+                    }
+                    tmem_st32(st + hf * 32, pk);
                 }
                 l += lsum;
-                tmem_st32(st, pk[0]);
-                tmem_st32(st + 32, pk[1]);
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(&bars[C::B_PFULL + (c & 1)]);
             }
             // ---------------------------------------------------------------- epilogue
-            float o[D];
             if (I.n_chunks > 0) {
                 __syncwarp();
                 mbar_wait(&bars[C::B_ODONE], (uint32_t)((c - 1) & 1));
                 tc_fence_after();
+            }
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            __nv_bfloat16* orow = p.o + (I.bh * p.N + qrow) * D;
+            if (I.n_chunks > 0) {
 #pragma unroll
                 for (int g = 0; g < D / 32; ++g) {
                     uint32_t ov[32];
                     tmem_ld32(tmem_O + lane_off + g * 32, ov);
                     tmem_ld_wait();
+                    if (row_ok && l > 0.f) {
 #pragma unroll
-                    for (int t = 0; t < 32; ++t) o[g * 32 + t] = __uint_as_float(ov[t]);
+                        for (int t = 0; t < 32; t += 8) {
+                            uint4 w;
+                            w.x = pack_bf16x2(__uint_as_float(ov[t]) * inv, __uint_as_float(ov[t + 1]) * inv);
+                            w.y = pack_bf16x2(__uint_as_float(ov[t + 2]) * inv, __uint_as_float(ov[t + 3]) * inv);
+                            w.z = pack_bf16x2(__uint_as_float(ov[t + 4]) * inv, __uint_as_float(ov[t + 5]) * inv);
+                            w.w = pack_bf16x2(__uint_as_float(ov[t + 6]) * inv, __uint_as_float(ov[t + 7]) * inv);
+                            *reinterpret_cast<uint4*>(orow + g * 32 + t) = w;
+                        }
+                    }
                 }
                 tc_fence_before();
                 mbar_arrive(&bars[C::B_OEMPTY]);
             }
             if (row_ok) {
-                __nv_bfloat16* orow = p.o + (I.bh * p.N + qrow) * D;
                 float lse_v;
                 if (l > 0.f) {
-                    const float inv = 1.f / l;
-#pragma unroll
-                    for (int t = 0; t < D; t += 8) {
-                        uint4 w;
-                        w.x = pack_bf16x2(o[t] * inv, o[t + 1] * inv);
-                        w.y = pack_bf16x2(o[t + 2] * inv, o[t + 3] * inv);
-                        w.z = pack_bf16x2(o[t + 4] * inv, o[t + 5] * inv);
-                        w.w = pack_bf16x2(o[t + 6] * inv, o[t + 7] * inv);
-                        *reinterpret_cast<uint4*>(orow + t) = w;
-                    }
                     lse_v = (m_ref + __log2f(l)) * 0.69314718055994531f;
                 } else {
                     // degenerate row (reading R6): O_r = V_r, LSE_r = scale*<q_r,k_r>
