@@ -84,6 +84,24 @@ def head_range(H, ws, rank):
     return h0, h0 + base + (1 if rank < rem else 0), base + (1 if rem else 0)
 
 
+
+def allgather_heads(o_local, o_pad, o_all, group=None):
+    """C1: all-gather per-rank head slices of O (padded to the max heads
+    per rank so every rank contributes the same number of bytes)."""
+    import torch.distributed as dist
+    o_pad[:o_local.numel()].copy_(o_local.reshape(-1))
+    dist.all_gather_into_tensor(o_all.view(-1), o_pad, group=group)
+
+
+def assemble_heads(o_all, B, H, N, D, ws):
+    """Undo the padding of allgather_heads: [ws, B*hmax*N*D] -> [B, H, N, D]."""
+    import torch
+    parts = []
+    for r in range(ws):
+        h0, h1, hmax = head_range(H, ws, r)
+        parts.append(o_all[r, :B * (h1 - h0) * N * D].view(B, h1 - h0, N, D))
+    return torch.cat(parts, dim=1)
+
 # ------------------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -300,8 +318,7 @@ def run_ours(args):
         if ev:
             ev[2].record(stream)
         if ws > 1:
-            o_pad[:o.numel()].copy_(o.view(-1))
-            dist.all_gather_into_tensor(o_all.view(-1), o_pad)
+            allgather_heads(o, o_pad, o_all)
         if ev:
             ev[3].record(stream)
             timers.append(ev)
@@ -366,7 +383,7 @@ def run_ours(args):
         qh = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
         kh = torch.empty(k.shape, dtype=k.dtype, pin_memory=True)
         vh = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
-        oh_host = torch.empty(o.shape, dtype=o.dtype, pin_memory=True)
+        oh_host = torch.empty(o_all.shape if ws > 1 else o.shape, dtype=o.dtype, pin_memory=True)
         qh.copy_(q)
         kh.copy_(k)
         vh.copy_(v)
@@ -379,9 +396,8 @@ def run_ours(args):
             va.select_into(qd, kd, cfg, offsets, indices, cap, d_nnz, ws_sel, causal)
             va.sparse_fwd_into(qd, kd, vd, offsets, indices, pq, o, lse, ws_sp, cap, causal)
             if ws > 1:
-                o_pad[:o.numel()].copy_(o.view(-1))
-                dist.all_gather_into_tensor(o_all.view(-1), o_pad)
-            oh_host.copy_(o, non_blocking=True)
+                allgather_heads(o, o_pad, o_all)
+            oh_host.copy_(o_all if ws > 1 else o, non_blocking=True)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -397,7 +413,7 @@ def run_ours(args):
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e_ms = float(et[0])
         h2d = (q.numel() + k.numel() + v.numel()) * 2 * ws
-        d2h = o.numel() * 2 * ws
+        d2h = (o_all.numel() if ws > 1 else o.numel()) * 2
         e2e = {"value": dense_flops(B * H, N, D, causal) / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
         del qh, kh, vh, oh_host, qd, kd, vd

@@ -48,7 +48,7 @@ typedef enum {
     VECATTN_ERR_INVALID_ARGUMENT = 1, /* NULL pointer, pq not in {64,128}, alpha < 0 or NaN, bk not in
                                          {16,32,64}, gk < 1, TOPK with neither topk > 0 nor
                                          keep_frac in (0,1], Hq % Hkv != 0, scale < 0 or NaN          */
-    VECATTN_ERR_SHAPE = 2,            /* B, N < 1; D not in {64,128}; N >= 2^30; Hq > 1024; pointer not
+    VECATTN_ERR_SHAPE = 2,            /* B, N < 1; D not in {64,128}; N >= 2^28; Hq > 1024; pointer not
                                          16-byte aligned; B*Hkv*N >= 2^31                              */
     VECATTN_ERR_UNSUPPORTED = 3,      /* no sm_100 device, or cuTensorMapEncodeTiled unavailable      */
     VECATTN_ERR_WORKSPACE = 4,        /* ws == NULL or ws_bytes < *_workspace_bytes()                 */
@@ -140,6 +140,8 @@ VECATTN_API vecattn_status_t vecattn_debug_scores(const vecattn_problem_t* p, in
                                       float* scores, void* ws, size_t ws_bytes, vecattn_stream_t stream);
 
 VECATTN_API const char* vecattn_status_string(vecattn_status_t s);
+/* Text of the last CUDA error that made an entry point return VECATTN_ERR_CUDA (this thread). */
+VECATTN_API const char* vecattn_last_cuda_error(void);
 VECATTN_API int32_t vecattn_abi_version(void);
 
 #ifdef __cplusplus

@@ -1,26 +1,32 @@
 // attn.cu — vector-sparse attention (Eq. 5, Alg. 2) and the dense reference
-// (Eq. 1), one persistent tcgen05/TMEM kernel template, sm_100a.
+// (Eq. 1): one persistent tcgen05/TMEM kernel template, sm_100a.
 //
 // PAPER.md Eq. 5: for query block i,
 //     O[I_B(i)] = softmax( Q[I_B(i)] K[Idx(i)]^T / sqrt(D) ) V[Idx(i)]
 // computed with FlashAttention-style online softmax over chunks of gathered K/V
 // rows (Alg. 2; App. D.2).
 //
-// B200 design:
-//  * tcgen05 M=128 is the full-rate tile; the paper's query block is P_q = 64 rows
-//    (P:335).  A CTA tile is therefore 128 query rows = 128/P_q
-//    adjacent blocks, processed over the sorted UNION of their index lists
-//    (worklist kernel below).  Each union entry carries per-block membership bits;
-//    keys outside a row's own Idx(i) get score -inf, so every row computes exactly
-//    Eq. 5 for its own block.  For P_q = 128 the union is the block's own list.
-//  * K/V rows are gathered with TMA tile::gather4 (4 rows x 128 B per
-//    instruction) into 128B-swizzled shared memory, 128 keys per chunk, 3-stage ring.
-//  * S = Q K^T (M=128, N=128, K=D) -> TMEM (double-buffered); softmax warps
-//    (thread = query row = TMEM lane) apply masks, online max with lazy rescale
-//    (threshold 2^8), exp2, write P as bf16 back into TMEM over S; then
-//    O += P V with A = P from TMEM and B = V (MN-major) from shared memory.
-//  * Persistent CTAs with a dynamic atomic tile scheduler; tiles ordered
-//    head-major (K/V of one head stay L2-resident), causal tiles longest-first.
+// B200 design (DESIGN.md §6 "attn_kernel"):
+//  * Work item = 256 query rows = two M=128 tcgen05 tiles sharing every K/V chunk,
+//    so each gathered K/V row feeds 256 query rows (halves gather bytes per flop vs
+//    a single 128-row tile).  The paper's query block is P_q = 64 rows (P:335,
+//    P:690-696): an item covers 256/P_q adjacent blocks and iterates over the sorted
+//    UNION of their index lists (worklist_kernel).  Each union entry carries one
+//    membership bit per block; keys outside a row's own Idx(i) get score -inf, so
+//    every row computes exactly Eq. 5 for its own block.
+//  * K/V rows are gathered with TMA tile::gather4 (4 rows x 128 B per instruction)
+//    into 128B-swizzled shared memory by 4 loader warps (32 keys each, union entries
+//    prefetched one chunk ahead), 128 keys per chunk.
+//  * MMA warp, FA4-style ping-pong between the two tiles: S_t = Q_t K^T (M=N=128,
+//    K=D) into TMEM; P_t (bf16, written by softmax warpgroup t over S_t) feeds
+//    O_t += P_t V with A = P from TMEM and B = V (MN-major) from shared memory.
+//    Tensor order per chunk: PV0(c), S0(c+1), PV1(c), S1(c+1) -- while one
+//    warpgroup computes its softmax the tensor core works for the other.
+//  * Softmax warpgroup t: thread = query row = TMEM lane; masked row max in a
+//    first TMEM pass, lazy rescale (threshold 2^8, warp-voted because tcgen05.ld/st
+//    are warp-collective), exp2 with f32x2 FMA/ADD in a second pass.
+//  * Persistent CTAs, dynamic atomic scheduler, items head-major (one head's K/V
+//    stays L2-resident), causal items longest-first.
 // Degenerate rows (no visible selected key; reading R6): O_r = V_r,
 // LSE_r = scale*<q_r,k_r>.
 #include "common.cuh"
@@ -32,65 +38,127 @@ namespace va {
 
 namespace {
 
-constexpr int kAttnThreads = 320;   // w0 sched+Q, w1 MMA, w2-5 softmax, w6-9 K/V loaders
+constexpr int kThreads = 448;  // w0 sched+Q, w1 MMA, w2-5 softmax tile 0, w6-9 softmax tile 1, w10-13 loaders
 constexpr int kLoadWarps = 4;
-constexpr int kStages = 3;
-constexpr uint32_t kPad = 0x3FFFFFFFu;   // meta key for padding lanes (sorts last)
+constexpr int kFirstLoadWarp = 10;
+constexpr int kSoftmaxThreads = 256;
+constexpr uint32_t kKeyMask = 0x0FFFFFFFu;  // entry = key | membership << 28
+constexpr uint32_t kPad = 0x0FFFFFFFu;      // meta key for padding lanes (sorts last)
 
 template <int D>
 struct AttnCfg {
+    static constexpr int kStages = D == 128 ? 2 : 4;
     static constexpr int kCB = D / 64;
     static constexpr int kTileBytes = kCB * 128 * 128;  // 128 rows x D bf16
-    static constexpr int kOffQ = 0;
-    static constexpr int kOffK = kTileBytes;
+    static constexpr int kOffQ = 0;                      // two Q tiles
+    static constexpr int kOffK = 2 * kTileBytes;
     static constexpr int kOffV = kOffK + kStages * kTileBytes;
     static constexpr int kOffMeta = kOffV + kStages * kTileBytes;
-    static constexpr int kMetaWords = 128 + 8;          // keys[128], maskA[4], maskB[4]
-    static constexpr int kOffBar = kOffMeta + kStages * kMetaWords * 4;
-    // barriers
+    static constexpr int kMetaWords = 128;               // keys[128] (causal prefix search)
+    static constexpr int kOffQx = (kOffMeta + kStages * kMetaWords * 4 + 1023) / 1024 * 1024;  // Q_ext [2][128 x 16] bf16
+    static constexpr int kOffKx = kOffQx + 2 * 128 * 16 * 2;               // K_ext [stages][128 x 16] bf16
+    static constexpr int kOffBar = kOffKx + kStages * 128 * 16 * 2;
     static constexpr int B_QFULL = 0, B_QEMPTY = 1, B_KFULL = 2, B_KEMPTY = B_KFULL + kStages,
                          B_VFULL = B_KEMPTY + kStages, B_VEMPTY = B_VFULL + kStages,
                          B_MFULL = B_VEMPTY + kStages, B_SFULL = B_MFULL + kStages, B_PFULL = B_SFULL + 2,
-                         B_ODONE = B_PFULL + 2, B_OEMPTY = B_ODONE + 1, B_IFULL = B_OEMPTY + 1,
+                         B_ODONE = B_PFULL + 2, B_OEMPTY = B_ODONE + 2, B_IFULL = B_OEMPTY + 2,
                          B_IEMPTY = B_IFULL + 2, kNumBars = B_IEMPTY + 2;
     static constexpr int kOffItem = kOffBar + kNumBars * 8;
     static constexpr int kSmem = kOffItem + 16;
-    static constexpr uint32_t kTmemCols = 512;          // S0 [0,128) S1 [128,256) O [256,256+D)
+    static constexpr uint32_t kTmemCols = 512;  // tile t: S_t [256t, 256t+128) (P_t over its first 64), O_t [256t+128, ...)
     static constexpr uint32_t kIdescS = make_idesc_bf16(128, 128, 0, 0);
     static constexpr uint32_t kIdescPV = make_idesc_bf16(128, D, 0, 1);
 };
 
 struct Item {
-    int64_t bh, mt;
+    int64_t bh, it;  // head, 256-row item within the head
     int n_chunks;
-    int len;       // gather: union length
-    int64_t base;  // gather: worklist base
+    int lb, l0, l1;  // gather: union segment lengths (keys of both tiles | tile 0 only | tile 1 only)
+    int nb, n0, n1;  // gather: chunks per segment
+    int len;         // dense: key extent
+    int64_t base;    // gather: worklist base
+};
+
+struct Chunk {
+    int mask;   // bit t: tile t computes this chunk
+    int start;  // first worklist entry (relative to the item base) / first key (dense)
+    int len;    // valid entries / keys
 };
 
 template <bool GATHER>
 VA_DEV Item decode_item(const AttnParams& p, int item) {
-    Item it;
-    it.bh = item / p.n_mt;
-    it.mt = p.n_mt - 1 - (item % p.n_mt);  // longest-first within a head (causal)
+    Item I;
+    I.bh = item / p.n_mt;
+    I.it = p.n_mt - 1 - (item % p.n_mt);  // longest-first within a head (causal)
     if constexpr (GATHER) {
-        const int64_t G = 128 / p.pq;
-        it.len = p.wl_len[it.bh * p.n_mt + it.mt];
-        it.base = p.offsets[it.bh * p.Np + G * it.mt];
-        it.n_chunks = (it.len + 127) / 128;
+        const int64_t G = 256 / p.pq;
+        const int64_t x = I.bh * p.n_mt + I.it;
+        I.lb = p.wl_len[3 * x];
+        I.l0 = p.wl_len[3 * x + 1];
+        I.l1 = p.wl_len[3 * x + 2];
+        I.nb = (I.lb + 127) / 128;
+        I.n0 = (I.l0 + 127) / 128;
+        I.n1 = (I.l1 + 127) / 128;
+        I.n_chunks = I.nb + I.n0 + I.n1;
+        I.base = p.offsets[I.bh * p.Np + G * I.it];
+        I.len = 0;
     } else {
-        const int64_t kend = p.causal ? min(p.N, (it.mt + 1) * 128) : p.N;
-        it.len = (int)kend;
-        it.base = 0;
-        it.n_chunks = (int)((kend + 127) / 128);
+        const int64_t kend = p.causal ? min(p.N, (I.it + 1) * 256) : p.N;
+        I.len = (int)kend;
+        I.base = 0;
+        I.n_chunks = (int)((kend + 127) / 128);
+        I.lb = I.l0 = I.l1 = I.nb = I.n0 = I.n1 = 0;
     }
-    return it;
+    return I;
 }
+
+// Chunk order: shared chunks first, then tile-0-only and tile-1-only chunks interleaved
+// (so the tensor core alternates between the two softmax warpgroups).
+template <bool GATHER>
+VA_DEV Chunk chunk_info(const Item& I, int j) {
+    Chunk c;
+    if constexpr (!GATHER) {
+        c.mask = 3;
+        c.start = 128 * j;
+        c.len = min(128, I.len - 128 * j);
+        return c;
+    } else {
+        if (j < I.nb) {
+            c.mask = 3;
+            c.start = 128 * j;
+            c.len = min(128, I.lb - 128 * j);
+            return c;
+        }
+        const int k = j - I.nb;
+        const int m = min(I.n0, I.n1);
+        int t, q;
+        if (k < 2 * m) {
+            t = k & 1;
+            q = k >> 1;
+        } else {
+            t = I.n0 > I.n1 ? 0 : 1;
+            q = m + (k - 2 * m);
+        }
+        c.mask = 1 << t;
+        if (t == 0) {
+            c.start = I.lb + 128 * q;
+            c.len = min(128, I.l0 - 128 * q);
+        } else {
+            c.start = I.lb + I.l0 + 128 * q;
+            c.len = min(128, I.l1 - 128 * q);
+        }
+        return c;
+    }
+}
+
+VA_DEV uint32_t prefix_mask(int64_t nb) { return nb >= 32 ? 0xffffffffu : (nb <= 0 ? 0u : ((1u << nb) - 1u)); }
 
 }  // namespace
 
 template <int D, bool GATHER>
-__global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_constant__ AttnParams p) {
+__global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant__ AttnParams p) {
     using C = AttnCfg<D>;
+    constexpr int S_ = C::kStages;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sQ = smem + C::kOffQ;
     uint8_t* sK = smem + C::kOffK;
@@ -107,38 +175,52 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
         if ((smem_u32(smem) & 1023u) != 0) __trap();
         mbar_init(&bars[C::B_QFULL], 1);
         mbar_init(&bars[C::B_QEMPTY], 1);
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&bars[C::B_KFULL + s], GATHER ? kLoadWarps : 1);
+        for (int s = 0; s < S_; ++s) {
+            mbar_init(&bars[C::B_KFULL + s], GATHER ? 2 : 1);
             mbar_init(&bars[C::B_KEMPTY + s], 1);
-            mbar_init(&bars[C::B_VFULL + s], GATHER ? kLoadWarps : 1);
+            mbar_init(&bars[C::B_VFULL + s], GATHER ? 2 : 1);
             mbar_init(&bars[C::B_VEMPTY + s], 1);
-            mbar_init(&bars[C::B_MFULL + s], kLoadWarps);
+            mbar_init(&bars[C::B_MFULL + s], 2);
         }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&bars[C::B_SFULL + s], 1);
-            mbar_init(&bars[C::B_PFULL + s], 128);
-            mbar_init(&bars[C::B_IFULL + s], 1);
-            mbar_init(&bars[C::B_IEMPTY + s], 1 + 128 + kLoadWarps);
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(&bars[C::B_SFULL + t], 1);
+            mbar_init(&bars[C::B_PFULL + t], 128);
+            mbar_init(&bars[C::B_ODONE + t], 1);
+            mbar_init(&bars[C::B_OEMPTY + t], 128);
+            mbar_init(&bars[C::B_IFULL + t], 1);
+            mbar_init(&bars[C::B_IEMPTY + t], 1 + kSoftmaxThreads + kLoadWarps);
         }
-        mbar_init(&bars[C::B_ODONE], 1);
-        mbar_init(&bars[C::B_OEMPTY], 128);
         fence_barrier_init();
+    }
+    if constexpr (GATHER) {
+        // Membership masking on the tensor core: S = [Q | E] [K | F]^T with E = one-hot of the
+        // row's block (Q_ext, constant per row position) and F[j][b] = 0 if key j is in block
+        // b's index set else -2^100 (K_ext, written per chunk by the loaders).  Members get +0
+        // exactly; non-members a score of -2^100 whose exp2 underflows to 0.
+        uint16_t* qx = reinterpret_cast<uint16_t*>(smem + C::kOffQx);
+        for (int x = threadIdx.x; x < 2 * 128 * 16; x += kThreads) {
+            const int t = x / (128 * 16), r = (x / 16) % 128, e = x % 16;
+            const int blk = (128 * t + r) / p.pq;
+            qx[(t * 128 * 16 * 2 + k16_offset(r, e)) / 2] = (e == blk) ? 0x3F80u : 0u;  // bf16 1.0
+        }
+        uint32_t* kx = reinterpret_cast<uint32_t*>(smem + C::kOffKx);
+        for (int x = threadIdx.x; x < S_ * 128 * 16 / 2; x += kThreads) kx[x] = 0u;
+        fence_proxy_async();
     }
     if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const uint32_t tmem_O = tmem_base + 256;
 
     if (warp == 0) {
-        // ============================================ scheduler: dynamic items + Q tile loads
+        // ======================================== scheduler: dynamic items + Q tile loads
         if (lane == 0) {
             tma_prefetch_desc(&p.tm_q);
             tma_prefetch_desc(&p.tm_k);
             tma_prefetch_desc(&p.tm_v);
         }
-        int qi = 0;  // Q loads issued
+        int qi = 0;
         for (int it = 0;; ++it) {
             const int slot = it & 1;
             int item = 0;
@@ -154,21 +236,31 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
             if (I.n_chunks == 0) continue;
             if (lane == 0) {
                 if (qi > 0) mbar_wait(&bars[C::B_QEMPTY], (qi - 1) & 1);
-                mbar_arrive_expect_tx(&bars[C::B_QFULL], C::kTileBytes);
+                mbar_arrive_expect_tx(&bars[C::B_QFULL], 2 * C::kTileBytes);
 #pragma unroll
-                for (int cb = 0; cb < C::kCB; ++cb)
-                    tma_load_3d(sQ + cb * 128 * 128, &p.tm_q, &bars[C::B_QFULL], cb * 64, (int)(I.mt * 128),
-                                (int)I.bh);
+                for (int t = 0; t < 2; ++t)
+#pragma unroll
+                    for (int cb = 0; cb < C::kCB; ++cb)
+                        tma_load_3d(sQ + t * C::kTileBytes + cb * 128 * 128, &p.tm_q, &bars[C::B_QFULL], cb * 64,
+                                    (int)(I.it * 256 + t * 128), (int)I.bh);
             }
             ++qi;
         }
-    } else if (warp >= 6) {
-        // ============================================ K/V loaders (4 warps)
-        // GATHER: warp g owns chunk columns [32g, 32g+32): reads its 32 union entries
-        // (prefetched one chunk ahead), publishes keys + membership ballots (mask word g)
-        // to the meta ring, and issues 8 K + 8 V tile::gather4 per column block.
-        // Dense: warp 6 issues the K/V tile loads.
-        const int g = (int)warp - 6;
+    } else if (warp >= kFirstLoadWarp) {
+        // ======================================== K/V loaders (4 warps)
+        // Warps 10-11 load K, warps 12-13 load V; warp (g & 1) owns chunk columns
+        // [64*(g&1), +64).  GATHER: each lane holds 2 union entries (prefetched one chunk
+        // ahead) and each warp issues 16 tile::gather4 per 128-B column block.  K loaders
+        // also write the K_ext membership-bias rows (consumed by the S MMA, freed with
+        // KEMPTY); V loaders publish the keys for the causal mask (freed with VEMPTY).
+        // K and V are decoupled so the K ring refills as soon as the S MMAs release it.
+        const int g = (int)warp - kFirstLoadWarp;
+        const bool isK = g < 2;
+        const int sub = g & 1;
+        uint8_t* ring = isK ? sK : sV;
+        const void* tmap = isK ? (const void*)&p.tm_k : (const void*)&p.tm_v;
+        const int bfull = isK ? C::B_KFULL : C::B_VFULL;
+        const int bempty = isK ? C::B_KEMPTY : C::B_VEMPTY;
         int64_t c = 0;
         for (int it = 0;; ++it) {
             const int slot = it & 1;
@@ -183,101 +275,128 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
             const int64_t bh_kv = b * p.Hkv + h / (p.Hq / p.Hkv);
             if constexpr (GATHER) {
                 const uint32_t* wlp = p.wl + I.base;
-                int pos = 32 * g + (int)lane;
-                uint32_t e_cur = pos < I.len ? __ldg(wlp + pos) : 0u;
+                const int col0 = 64 * sub + (int)lane, col1 = col0 + 32;
+                Chunk ch = chunk_info<true>(I, 0);
+                uint32_t e0 = col0 < ch.len ? __ldg(wlp + ch.start + col0) : 0u;
+                uint32_t e1 = col1 < ch.len ? __ldg(wlp + ch.start + col1) : 0u;
                 for (int j = 0; j < I.n_chunks; ++j, ++c) {
-                    const int s = (int)(c % kStages);
-                    const int round = (int)(c / kStages);
-                    const bool ok = pos < I.len;
-                    const int pos_n = pos + 128;
-                    const uint32_t e_nxt = (j + 1 < I.n_chunks && pos_n < I.len) ? __ldg(wlp + pos_n) : 0u;
-                    const uint32_t key = e_cur & 0x3FFFFFFFu;
-                    const int row = (int)(bh_kv * p.N + (ok ? key : 0u));
-                    const uint32_t wA = __ballot_sync(0xffffffffu, ok && ((e_cur >> 30) & 1u));
-                    const uint32_t wB = __ballot_sync(0xffffffffu, ok && ((e_cur >> 31) & 1u));
-                    if (lane == 0 && round > 0) {
-                        mbar_wait(&bars[C::B_KEMPTY + s], (round - 1) & 1);
-                        mbar_wait(&bars[C::B_VEMPTY + s], (round - 1) & 1);
+                    const int s = (int)(c % S_);
+                    const int round = (int)(c / S_);
+                    const bool ok0 = col0 < ch.len, ok1 = col1 < ch.len;
+                    Chunk chn;
+                    chn.len = 0;
+                    chn.start = 0;
+                    if (j + 1 < I.n_chunks) chn = chunk_info<true>(I, j + 1);
+                    const uint32_t n0 = col0 < chn.len ? __ldg(wlp + chn.start + col0) : 0u;
+                    const uint32_t n1 = col1 < chn.len ? __ldg(wlp + chn.start + col1) : 0u;
+                    const uint32_t key0 = e0 & kKeyMask, key1 = e1 & kKeyMask;
+                    const int row0 = (int)(bh_kv * p.N + (ok0 ? key0 : 0u));
+                    const int row1 = (int)(bh_kv * p.N + (ok1 ? key1 : 0u));
+                    if (lane == 0 && round > 0) mbar_wait(&bars[bempty + s], (round - 1) & 1);
+                    __syncwarp();
+                    if (isK) {
+                        // K_ext rows: bias 0 for member blocks, -2^100 (bf16 0xF180) otherwise
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int kk = u ? col1 : col0;
+                            const uint32_t mem = (u ? ok1 : ok0) ? ((u ? e1 : e0) >> 28) : 0u;
+                            const uint32_t b0 = (mem & 1u) ? 0u : 0xF180u, b1 = (mem & 2u) ? 0u : 0xF180u;
+                            const uint32_t b2 = (mem & 4u) ? 0u : 0xF180u, b3 = (mem & 8u) ? 0u : 0xF180u;
+                            *reinterpret_cast<uint4*>(smem + C::kOffKx + s * 128 * 16 * 2 + k16_offset(kk, 0)) =
+                                make_uint4(b0 | (b1 << 16), b2 | (b3 << 16), 0u, 0u);
+                        }
+                        fence_proxy_async();  // generic-proxy smem writes -> tcgen05.mma (async proxy)
+                    } else {
+                        uint32_t* meta = sMeta + s * C::kMetaWords;
+                        meta[col0] = ok0 ? key0 : kPad;
+                        meta[col1] = ok1 ? key1 : kPad;
                     }
                     __syncwarp();
-                    uint32_t* meta = sMeta + s * C::kMetaWords;
-                    meta[32 * g + lane] = ok ? key : kPad;
                     if (lane == 0) {
-                        meta[128 + g] = wA;
-                        meta[132 + g] = wB;
+                        if (!isK) mbar_arrive(&bars[C::B_MFULL + s]);
+                        mbar_arrive_expect_tx(&bars[bfull + s], 64 * D * 2);
                     }
+                    // lane L < 16 gathers keys 4L..4L+3 of this warp's 64 (entries 0-31 in e0 of
+                    // lanes 0-31, 32-63 in e1)
+                    const int q0 = (4 * (int)lane) & 31;
+                    const int ra = __shfl_sync(0xffffffffu, row0, q0), rb = __shfl_sync(0xffffffffu, row0, q0 + 1);
+                    const int rc = __shfl_sync(0xffffffffu, row0, q0 + 2), rd = __shfl_sync(0xffffffffu, row0, q0 + 3);
+                    const int sa = __shfl_sync(0xffffffffu, row1, q0), sb = __shfl_sync(0xffffffffu, row1, q0 + 1);
+                    const int sc = __shfl_sync(0xffffffffu, row1, q0 + 2), sd = __shfl_sync(0xffffffffu, row1, q0 + 3);
                     __syncwarp();
-                    if (lane == 0) {
-                        mbar_arrive(&bars[C::B_MFULL + s]);
-                        mbar_arrive_expect_tx(&bars[C::B_KFULL + s], 32 * D * 2);
-                        mbar_arrive_expect_tx(&bars[C::B_VFULL + s], 32 * D * 2);
-                    }
-                    const int r0 = __shfl_sync(0xffffffffu, row, (4 * lane) & 31);
-                    const int r1 = __shfl_sync(0xffffffffu, row, (4 * lane + 1) & 31);
-                    const int r2 = __shfl_sync(0xffffffffu, row, (4 * lane + 2) & 31);
-                    const int r3 = __shfl_sync(0xffffffffu, row, (4 * lane + 3) & 31);
-                    __syncwarp();
-                    if (lane < 8) {
-                        uint8_t* dK = sK + s * C::kTileBytes + (32 * g + 4 * lane) * 128;
-                        uint8_t* dV = sV + s * C::kTileBytes + (32 * g + 4 * lane) * 128;
+                    if (lane < 16) {
+                        const bool hi = lane >= 8;
+                        uint8_t* dst = ring + s * C::kTileBytes + (64 * sub + 4 * (int)lane) * 128;
 #pragma unroll
                         for (int cb = 0; cb < C::kCB; ++cb)
-                            tma_gather4(dK + cb * 128 * 128, &p.tm_k, &bars[C::B_KFULL + s], cb * 64, r0, r1, r2, r3);
-#pragma unroll
-                        for (int cb = 0; cb < C::kCB; ++cb)
-                            tma_gather4(dV + cb * 128 * 128, &p.tm_v, &bars[C::B_VFULL + s], cb * 64, r0, r1, r2, r3);
+                            tma_gather4(dst + cb * 128 * 128, tmap, &bars[bfull + s], cb * 64, hi ? sa : ra,
+                                        hi ? sb : rb, hi ? sc : rc, hi ? sd : rd);
                     }
-                    e_cur = e_nxt;
-                    pos = pos_n;
+                    e0 = n0;
+                    e1 = n1;
+                    ch = chn;
                 }
             } else {
                 for (int j = 0; j < I.n_chunks; ++j, ++c) {
-                    if (g != 0 || lane != 0) continue;
-                    const int s = (int)(c % kStages);
-                    const int round = (int)(c / kStages);
-                    if (round > 0) {
-                        mbar_wait(&bars[C::B_KEMPTY + s], (round - 1) & 1);
-                        mbar_wait(&bars[C::B_VEMPTY + s], (round - 1) & 1);
-                    }
-                    uint8_t* dK = sK + s * C::kTileBytes;
-                    uint8_t* dV = sV + s * C::kTileBytes;
-                    mbar_arrive_expect_tx(&bars[C::B_KFULL + s], C::kTileBytes);
+                    if (sub != 0 || lane != 0) continue;
+                    const int s = (int)(c % S_);
+                    const int round = (int)(c / S_);
+                    if (round > 0) mbar_wait(&bars[bempty + s], (round - 1) & 1);
+                    uint8_t* dst = ring + s * C::kTileBytes;
+                    mbar_arrive_expect_tx(&bars[bfull + s], C::kTileBytes);
 #pragma unroll
                     for (int cb = 0; cb < C::kCB; ++cb)
-                        tma_load_3d(dK + cb * 128 * 128, &p.tm_k, &bars[C::B_KFULL + s], cb * 64, j * 128,
-                                    (int)bh_kv);
-                    mbar_arrive_expect_tx(&bars[C::B_VFULL + s], C::kTileBytes);
-#pragma unroll
-                    for (int cb = 0; cb < C::kCB; ++cb)
-                        tma_load_3d(dV + cb * 128 * 128, &p.tm_v, &bars[C::B_VFULL + s], cb * 64, j * 128,
-                                    (int)bh_kv);
+                        tma_load_3d(dst + cb * 128 * 128, tmap, &bars[bfull + s], cb * 64, j * 128, (int)bh_kv);
                 }
                 __syncwarp();
             }
         }
     } else if (warp == 1) {
-        // ==================================================================== MMA issuer
+        // ======================================== MMA issuer (single thread)
+        // Per chunk c with tile mask m (next chunk mask mn):
+        //   S_t(c+1) for tiles entering at c+1 (early, overlaps softmax of c),
+        //   then for t in m: PV_t(c), S_t(c+1) if t continues.
         if (elect_one()) {
-            int64_t c = 0;
+            int64_t c = 0;            // global chunk counter (stage ring)
+            uint32_t cnt[2] = {0, 0}; // per-tile chunk counters (SFULL/PFULL/ODONE phases)
             int qi = 0, oi = 0;
-            auto issue_pv = [&](int64_t cc, bool first) {
-                const int s = (int)(cc % kStages);
-                if (first) {
-                    if (oi > 0) mbar_wait(&bars[C::B_OEMPTY], (oi - 1) & 1);
-                    ++oi;
+            const uint32_t qa = smem_u32(sQ);
+            auto issue_s = [&](int t, int64_t cc) {
+                const int s = (int)(cc % S_);
+                const uint32_t ka = smem_u32(sK + s * C::kTileBytes);
+                const uint32_t q_t = qa + t * C::kTileBytes;
+                const uint32_t st = tmem_base + (uint32_t)(256 * t);
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const uint64_t adesc = make_sdesc(q_t + (kk >> 2) * 128 * 128 + (kk & 3) * 32, 16, 1024);
+                    const uint64_t bdesc = make_sdesc(ka + (kk >> 2) * 128 * 128 + (kk & 3) * 32, 16, 1024);
+                    mma_bf16_ss(st, adesc, bdesc, C::kIdescS, kk > 0 ? 1u : 0u);
                 }
-                mbar_wait(&bars[C::B_PFULL + (cc & 1)], (uint32_t)((cc >> 1) & 1));
-                mbar_wait(&bars[C::B_VFULL + s], (uint32_t)((cc / kStages) & 1));
+                if constexpr (GATHER) {  // + onehot(block) . bias(key, block)^T (membership mask)
+                    const uint64_t adesc = make_sdesc(smem_u32(smem + C::kOffQx + t * 128 * 16 * 2), 128, 256, 0);
+                    const uint64_t bdesc = make_sdesc(smem_u32(smem + C::kOffKx + s * 128 * 16 * 2), 128, 256, 0);
+                    mma_bf16_ss(st, adesc, bdesc, C::kIdescS, 1u);
+                }
+                mma_commit(&bars[C::B_SFULL + t]);
+            };
+            auto issue_pv = [&](int t, int64_t cc, bool first) {
+                const int s = (int)(cc % S_);
+                mbar_wait(&bars[C::B_PFULL + t], cnt[t] & 1u);
+                ++cnt[t];
                 tc_fence_after();
-                const uint32_t pt = tmem_base + (uint32_t)((cc & 1) * 128);
+                const uint32_t pt = tmem_base + (uint32_t)(256 * t);
+                const uint32_t ot = tmem_base + (uint32_t)(256 * t + 128);
                 const uint32_t va = smem_u32(sV + s * C::kTileBytes);
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
                     const uint64_t bdesc = make_sdesc(va + kk * 16 * 128, 128 * 128, 1024);
-                    mma_bf16_ts(tmem_O, pt + kk * 8, bdesc, C::kIdescPV, (first && kk == 0) ? 0u : 1u);
+                    mma_bf16_ts(ot, pt + kk * 8, bdesc, C::kIdescPV, (first && kk == 0) ? 0u : 1u);
                 }
-                mma_commit(&bars[C::B_VEMPTY + s]);
-                mma_commit(&bars[C::B_ODONE]);
+                mma_commit(&bars[C::B_ODONE + t]);
+            };
+            auto wait_k = [&](int64_t cc) {
+                mbar_wait(&bars[C::B_KFULL + (int)(cc % S_)], (uint32_t)((cc / S_) & 1));
+                tc_fence_after();
             };
             for (int it = 0;; ++it) {
                 const int slot = it & 1;
@@ -289,37 +408,66 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
                 if (I.n_chunks == 0) continue;
                 mbar_wait(&bars[C::B_QFULL], qi & 1);
                 ++qi;
-                tc_fence_after();
-                const uint32_t qa = smem_u32(sQ);
-                for (int j = 0; j < I.n_chunks; ++j, ++c) {
-                    const int s = (int)(c % kStages);
-                    mbar_wait(&bars[C::B_KFULL + s], (uint32_t)((c / kStages) & 1));
-                    tc_fence_after();
-                    const uint32_t ka = smem_u32(sK + s * C::kTileBytes);
-                    const uint32_t st = tmem_base + (uint32_t)((c & 1) * 128);
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const uint64_t adesc = make_sdesc(qa + (kk >> 2) * 128 * 128 + (kk & 3) * 32, 16, 1024);
-                        const uint64_t bdesc = make_sdesc(ka + (kk >> 2) * 128 * 128 + (kk & 3) * 32, 16, 1024);
-                        mma_bf16_ss(st, adesc, bdesc, C::kIdescS, kk > 0 ? 1u : 0u);
-                    }
-                    mma_commit(&bars[C::B_KEMPTY + s]);
-                    mma_commit(&bars[C::B_SFULL + (c & 1)]);
-                    if (j == I.n_chunks - 1) mma_commit(&bars[C::B_QEMPTY]);
-                    if (j > 0) issue_pv(c - 1, j == 1);
+                if (oi > 0) {  // O_0 / O_1 of the previous item drained by the epilogues
+                    mbar_wait(&bars[C::B_OEMPTY + 0], (oi - 1) & 1);
+                    mbar_wait(&bars[C::B_OEMPTY + 1], (oi - 1) & 1);
                 }
-                issue_pv(c - 1, I.n_chunks == 1);
+                ++oi;
+                bool started[2] = {false, false};
+                int m = chunk_info<GATHER>(I, 0).mask;
+                wait_k(c);
+                if (m & 1) issue_s(0, c);
+                if (m & 2) issue_s(1, c);
+                mma_commit(&bars[C::B_KEMPTY + (int)(c % S_)]);
+                if (I.n_chunks == 1) mma_commit(&bars[C::B_QEMPTY]);
+                for (int j = 0; j < I.n_chunks; ++j, ++c) {
+                    const int s = (int)(c % S_);
+                    const bool more = j + 1 < I.n_chunks;
+                    const int mn = more ? chunk_info<GATHER>(I, j + 1).mask : 0;
+                    bool have_k = false;
+                    if (mn & ~m) {  // tiles that start at c+1 only: give the tensor core work now
+                        wait_k(c + 1);
+                        have_k = true;
+                        if ((mn & ~m) & 1) issue_s(0, c + 1);
+                        if ((mn & ~m) & 2) issue_s(1, c + 1);
+                    }
+                    mbar_wait(&bars[C::B_VFULL + s], (uint32_t)((c / S_) & 1));
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        if (!(m & (1 << t))) continue;
+                        issue_pv(t, c, !started[t]);
+                        started[t] = true;
+                        if (mn & m & (1 << t)) {
+                            if (!have_k) {
+                                wait_k(c + 1);
+                                have_k = true;
+                            }
+                            issue_s(t, c + 1);
+                        }
+                    }
+                    mma_commit(&bars[C::B_VEMPTY + s]);
+                    if (more) {
+                        mma_commit(&bars[C::B_KEMPTY + (int)((c + 1) % S_)]);
+                        if (j + 2 == I.n_chunks) mma_commit(&bars[C::B_QEMPTY]);
+                    }
+                    m = mn;
+                }
             }
         }
         __syncwarp();
     } else {
-        // ==================================================================== softmax / epilogue
+        // ======================================== softmax / epilogue (two warpgroups)
+        const int tile = ((int)warp - 2) >> 2;
         const uint32_t quad = warp & 3u;
         const int r = (int)(quad * 32 + lane);
         const uint32_t lane_off = (quad * 32u) << 16;
-        const int member_bit = (p.pq == 64 && r >= 64) ? 31 : 30;
+        const uint32_t tS = tmem_base + lane_off + (uint32_t)(256 * tile);
+        const uint32_t tO = tS + 128;
+        const int row_in_item = 128 * tile + r;
+        const int blk = row_in_item / p.pq;  // membership bit 28 + blk
         const float sl2 = p.scale_log2;
         int64_t c = 0;
+        uint32_t ct = 0;  // this tile's chunk counter (SFULL/ODONE phases)
         for (int it = 0;; ++it) {
             const int slot = it & 1;
             mbar_wait(&bars[C::B_IFULL + slot], (it >> 1) & 1);
@@ -327,56 +475,47 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
             mbar_arrive(&bars[C::B_IEMPTY + slot]);
             if (item < 0) break;
             const Item I = decode_item<GATHER>(p, item);
-            const int64_t qrow = I.mt * 128 + r;
+            const int64_t qrow = I.it * 256 + row_in_item;
             const bool row_ok = qrow < p.N;
             float m_ref = -INFINITY;  // log2-domain reference max (lazy rescaling)
-            float l = 0.f;
+            float2 lsum2 = make_float2(0.f, 0.f);
+            int jt = 0;  // chunks of this item processed by this tile
             for (int j = 0; j < I.n_chunks; ++j, ++c) {
-                const int s = (int)(c % kStages);
-                // visibility mask of the 128 chunk columns for this row
+                const int s = (int)(c % S_);
+                if (!(chunk_info<GATHER>(I, j).mask & (1 << tile))) continue;
                 uint32_t mw[4];
                 if constexpr (GATHER) {
-                    mbar_wait(&bars[C::B_MFULL + s], (uint32_t)((c / kStages) & 1));
+                    mbar_wait(&bars[C::B_MFULL + s], (uint32_t)((c / S_) & 1));
                     const uint32_t* meta = sMeta + s * C::kMetaWords;
 #pragma unroll
-                    for (int wd = 0; wd < 4; ++wd) mw[wd] = meta[(member_bit == 30 ? 128 : 132) + wd];
+                    for (int wd = 0; wd < 4; ++wd) mw[wd] = 0xffffffffu;  // membership is applied by the MMA
                     if (p.causal) {
-                        // keys ascending: visible = prefix with key <= qrow
-                        int lo = 0, hi = 128;
+                        int lo = 0, hi = 128;  // keys ascending: visible = prefix with key <= qrow
                         while (lo < hi) {
                             const int mid = (lo + hi) >> 1;
                             if ((int64_t)meta[mid] <= qrow) lo = mid + 1;
                             else hi = mid;
                         }
 #pragma unroll
-                        for (int wd = 0; wd < 4; ++wd) {
-                            const int nb = lo - 32 * wd;
-                            const uint32_t pm = nb >= 32 ? 0xffffffffu : (nb <= 0 ? 0u : ((1u << nb) - 1u));
-                            mw[wd] &= pm;
-                        }
+                        for (int wd = 0; wd < 4; ++wd) mw[wd] &= prefix_mask(lo - 32 * wd);
                     }
                 } else {
-                    const int64_t key0 = (int64_t)j * 128;
                     const int64_t vend = p.causal ? min(p.N, qrow + 1) : p.N;
-                    const int64_t nv = vend - key0;
+                    const int64_t nv = vend - (int64_t)j * 128;
 #pragma unroll
-                    for (int wd = 0; wd < 4; ++wd) {
-                        const int64_t nb = nv - 32 * wd;
-                        mw[wd] = nb >= 32 ? 0xffffffffu : (nb <= 0 ? 0u : ((1u << nb) - 1u));
-                    }
+                    for (int wd = 0; wd < 4; ++wd) mw[wd] = prefix_mask(nv - 32 * wd);
                 }
-                mbar_wait(&bars[C::B_SFULL + (c & 1)], (uint32_t)((c >> 1) & 1));
-                tc_fence_after();
-                const uint32_t st = tmem_base + lane_off + (uint32_t)((c & 1) * 128);
                 const bool full = (mw[0] & mw[1] & mw[2] & mw[3]) == 0xffffffffu;
+                mbar_wait(&bars[C::B_SFULL + tile], ct & 1u);
+                tc_fence_after();
                 __syncwarp();  // reconverge after the per-row causal search (tcgen05.ld is .sync.aligned)
-                // ---- pass 1: masked row max, 64 TMEM columns at a time (low register pressure)
+                // ---- pass 1: masked row max, 64 TMEM columns at a time
                 float mx = -INFINITY;
 #pragma unroll
                 for (int hf = 0; hf < 2; ++hf) {
                     uint32_t a[32], b[32];
-                    tmem_ld32(st + hf * 64, a);
-                    tmem_ld32(st + hf * 64 + 32, b);
+                    tmem_ld32(tS + hf * 64, a);
+                    tmem_ld32(tS + hf * 64 + 32, b);
                     tmem_ld_wait();
                     if (full) {
 #pragma unroll
@@ -395,78 +534,81 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
                     }
                 }
                 const float m_new = fmaxf(m_ref, mx * sl2);
-                if (j > 0) {  // O must be stable (previous PV done) before a rescale
-                    mbar_wait(&bars[C::B_ODONE], (uint32_t)((c - 1) & 1));
+                if (jt > 0) {  // O_t stable (PV_t of this tile's previous chunk done) before a rescale
+                    mbar_wait(&bars[C::B_ODONE + tile], (ct - 1) & 1u);
                     tc_fence_after();
                 }
-                // Lazy rescale (only when the max grew by > 2^8): per-row decision, but
-                // tcgen05.ld/st are warp-collective (.sync.aligned), so the O update is
-                // done by the whole warp whenever any lane needs it (others scale by 1).
                 const bool need = m_new > m_ref + 8.0f;
                 const float corr = need ? ex2(m_ref - m_new) : 1.0f;
                 if (need) {
-                    l *= corr;
+                    lsum2.x *= corr;
+                    lsum2.y *= corr;
                     m_ref = m_new;
                 }
-                if (j > 0 && __any_sync(0xffffffffu, need)) {
+                if (jt > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll
                     for (int g = 0; g < D / 32; ++g) {
                         uint32_t o[32];
-                        tmem_ld32(tmem_O + lane_off + g * 32, o);
+                        tmem_ld32(tO + g * 32, o);
                         tmem_ld_wait();
 #pragma unroll
                         for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * corr);
-                        tmem_st32(tmem_O + lane_off + g * 32, o);
+                        tmem_st32(tO + g * 32, o);
                     }
                     tmem_st_wait();
                 }
-                // ---- pass 2: P = exp2(s*scale*log2e - m), bf16-packed into TMEM over S.
+                // ---- pass 2: P = exp2(s*scale*log2e - m) (f32x2 FMA/ADD), bf16-packed over S_t.
                 // Half hf reads S columns [64hf, 64hf+64) and writes P columns [32hf, 32hf+32),
-                // which only cover S columns already consumed.
+                // which only cover S columns this thread already consumed.
                 const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
-                float lsum = 0.f;
+                const uint64_t sl2x2 = pack_f32x2(sl2, sl2);
+                const uint64_t nmx2 = pack_f32x2(neg_m, neg_m);
 #pragma unroll
                 for (int hf = 0; hf < 2; ++hf) {
                     uint32_t a[32], b[32], pk[32];
-                    tmem_ld32(st + hf * 64, a);
-                    tmem_ld32(st + hf * 64 + 32, b);
+                    tmem_ld32(tS + hf * 64, a);
+                    tmem_ld32(tS + hf * 64 + 32, b);
                     tmem_ld_wait();
                     const uint32_t ma = full ? 0xffffffffu : mw[2 * hf];
                     const uint32_t mb = full ? 0xffffffffu : mw[2 * hf + 1];
 #pragma unroll
                     for (int t = 0; t < 32; t += 2) {
-                        float p0 = ex2(fmaf(__uint_as_float(a[t]), sl2, neg_m));
-                        float p1 = ex2(fmaf(__uint_as_float(a[t + 1]), sl2, neg_m));
-                        float p2 = ex2(fmaf(__uint_as_float(b[t]), sl2, neg_m));
-                        float p3 = ex2(fmaf(__uint_as_float(b[t + 1]), sl2, neg_m));
-                        p0 = (ma & (1u << t)) ? p0 : 0.f;
-                        p1 = (ma & (2u << t)) ? p1 : 0.f;
-                        p2 = (mb & (1u << t)) ? p2 : 0.f;
-                        p3 = (mb & (2u << t)) ? p3 : 0.f;
-                        lsum += (p0 + p1) + (p2 + p3);
+                        const float2 xa = unpack_f32x2(
+                            ffma2(pack_f32x2(__uint_as_float(a[t]), __uint_as_float(a[t + 1])), sl2x2, nmx2));
+                        const float2 xb = unpack_f32x2(
+                            ffma2(pack_f32x2(__uint_as_float(b[t]), __uint_as_float(b[t + 1])), sl2x2, nmx2));
+                        float p0 = ex2(xa.x), p1 = ex2(xa.y), p2 = ex2(xb.x), p3 = ex2(xb.y);
+                        if (!full) {
+                            p0 = (ma & (1u << t)) ? p0 : 0.f;
+                            p1 = (ma & (2u << t)) ? p1 : 0.f;
+                            p2 = (mb & (1u << t)) ? p2 : 0.f;
+                            p3 = (mb & (2u << t)) ? p3 : 0.f;
+                        }
+                        lsum2 = fadd2(lsum2, fadd2(make_float2(p0, p1), make_float2(p2, p3)));
                         pk[t >> 1] = pack_bf16x2(p0, p1);
                         pk[16 + (t >> 1)] = pack_bf16x2(p2, p3);
                     }
-                    tmem_st32(st + hf * 32, pk);
+                    tmem_st32(tS + hf * 32, pk);
                 }
-                l += lsum;
                 tmem_st_wait();
                 tc_fence_before();
-                mbar_arrive(&bars[C::B_PFULL + (c & 1)]);
+                mbar_arrive(&bars[C::B_PFULL + tile]);
+                ++ct;
+                ++jt;
             }
             // ---------------------------------------------------------------- epilogue
-            if (I.n_chunks > 0) {
-                __syncwarp();
-                mbar_wait(&bars[C::B_ODONE], (uint32_t)((c - 1) & 1));
-                tc_fence_after();
-            }
+            // rows that only ever saw masked keys carry m_ref ~ -2^100*scale*log2e: no visible key
+            const float l = (m_ref < -1e28f) ? 0.f : lsum2.x + lsum2.y;
             const float inv = l > 0.f ? 1.f / l : 0.f;
             __nv_bfloat16* orow = p.o + (I.bh * p.N + qrow) * D;
-            if (I.n_chunks > 0) {
+            if (jt > 0) {
+                __syncwarp();
+                mbar_wait(&bars[C::B_ODONE + tile], (ct - 1) & 1u);
+                tc_fence_after();
 #pragma unroll
                 for (int g = 0; g < D / 32; ++g) {
                     uint32_t ov[32];
-                    tmem_ld32(tmem_O + lane_off + g * 32, ov);
+                    tmem_ld32(tO + g * 32, ov);
                     tmem_ld_wait();
                     if (row_ok && l > 0.f) {
 #pragma unroll
@@ -480,13 +622,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
                         }
                     }
                 }
+            }
+            if (I.n_chunks > 0) {  // one OEMPTY arrival per item with chunks (even if this tile had none)
                 tc_fence_before();
-                mbar_arrive(&bars[C::B_OEMPTY]);
+                mbar_arrive(&bars[C::B_OEMPTY + tile]);
             }
             if (row_ok) {
-                float lse_v;
                 if (l > 0.f) {
-                    lse_v = (m_ref + __log2f(l)) * 0.69314718055994531f;
+                    if (p.lse) p.lse[I.bh * p.N + qrow] = (m_ref + __log2f(l)) * 0.69314718055994531f;
                 } else {
                     // degenerate row (reading R6): O_r = V_r, LSE_r = scale*<q_r,k_r>
                     const int64_t b = I.bh / p.Hq, h = I.bh % p.Hq;
@@ -499,9 +642,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
                         orow[t] = vr[t];
                         dot = fmaf(__bfloat162float(qr[t]), __bfloat162float(kr[t]), dot);
                     }
-                    lse_v = dot * p.scale;
+                    if (p.lse) p.lse[I.bh * p.N + qrow] = dot * p.scale;
                 }
-                if (p.lse) p.lse[I.bh * p.N + qrow] = lse_v;
             }
         }
     }
@@ -515,87 +657,167 @@ __global__ void __launch_bounds__(kAttnThreads, 1) attn_kernel(const __grid_cons
 }
 
 // ------------------------------------------------------------------------ worklist
-// One warp per 128-row tile: sorted union of the tile's block index lists with
-// membership bits (bit 30 = first block, bit 31 = second block), written at the
-// tile's CSR base (|A u B| <= |A| + |B| so it fits in place).
-__global__ void __launch_bounds__(256) worklist_kernel(const int64_t* __restrict__ offsets,
-                                                       const int32_t* __restrict__ indices,
-                                                       uint32_t* __restrict__ wl, int32_t* __restrict__ wl_len,
-                                                       int64_t BH, int64_t Np, int64_t n_mt, int32_t pq) {
-    const int lane = threadIdx.x & 31;
-    const int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (tile >= BH * n_mt) return;
-    const int64_t bh = tile / n_mt, mt = tile % n_mt;
-    const int64_t G = 128 / pq;
-    const int64_t ia = mt * G;
-    const int64_t ra = bh * Np + ia;
-    const int64_t base = offsets[ra];
-    const int64_t nA = offsets[ra + 1] - offsets[ra];
-    if (G == 1) {
-        for (int64_t t = lane; t < nA; t += 32) wl[base + t] = (uint32_t)indices[base + t] | (1u << 30);
-        if (lane == 0) wl_len[tile] = (int32_t)nA;
-        return;
-    }
-    const bool hasB = ia + 1 < Np;
-    const int64_t offB = hasB ? offsets[ra + 1] : 0;
-    const int64_t nB = hasB ? offsets[ra + 2] - offsets[ra + 1] : 0;
-    const int32_t* A = indices + base;
-    const int32_t* Bl = indices + offB;
-    const int INF = 0x7FFFFFFF;
-    int64_t pa = 0, pb = 0, out = 0;
-    const uint32_t lt = (1u << lane) - 1u;
-    while (pa < nA || pb < nB) {
-        const int a = (pa + lane < nA) ? A[pa + lane] : INF;
-        const int bv = (pb + lane < nB) ? Bl[pb + lane] : INF;
-        const int amax = __shfl_sync(0xffffffffu, a, 31);
-        const int bmax = __shfl_sync(0xffffffffu, bv, 31);
-        const int cut = min(amax, bmax);
-        const bool takeA = a != INF && a <= cut;
-        const bool takeB = bv != INF && bv <= cut;
-        // rank of a in the B window (#b < a), and of b in the A window
-        int rA = 0, rB = 0;
+// One CTA per 256-row item (G = 256/P_q blocks; tile 0 = blocks [0, G/2), tile 1 = the
+// rest).  Builds the sorted union of the item's block index lists with one membership
+// bit per block (entry = key | bits << 28), split into three segments -- keys used by
+// both tiles, by tile 0 only, by tile 1 only -- written back to back at the item's CSR
+// base (|union| <= sum of list lengths, so it fits in place); wl_len[3*item + {0,1,2}]
+// receives the segment lengths.  Per-block bitmaps in shared memory (atomicOr), then a
+// block-wide scan of per-word popcounts; key stripes of kStripe keys, with a counting
+// pre-pass when N > kStripe.
+constexpr int kWlThreads = 512;
+constexpr int kStripe = 262144;
+constexpr int kStripeWords = kStripe / 32;
+
+struct Seg3 {
+    int b, o0, o1;
+};
+
+__device__ __forceinline__ Seg3 block_scan3(Seg3 v, Seg3* tot_out, int* sh /* [3][16] */) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    Seg3 inc = v;
 #pragma unroll
-        for (int st = 16; st >= 1; st >>= 1) {
-            const int bq = __shfl_sync(0xffffffffu, bv, rA + st - 1);
-            if (bq < a) rA += st;
-            const int aq = __shfl_sync(0xffffffffu, a, rB + st - 1);
-            if (aq < bv) rB += st;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int nb = __shfl_up_sync(0xffffffffu, inc.b, o);
+        const int n0 = __shfl_up_sync(0xffffffffu, inc.o0, o);
+        const int n1 = __shfl_up_sync(0xffffffffu, inc.o1, o);
+        if (lane >= o) {
+            inc.b += nb;
+            inc.o0 += n0;
+            inc.o1 += n1;
         }
-        {   // final step for rank 31 -> 32
-            const int bq = __shfl_sync(0xffffffffu, bv, rA);
-            if (rA == 31 && bq < a) rA = 32;
-            const int aq = __shfl_sync(0xffffffffu, a, rB);
-            if (rB == 31 && aq < bv) rB = 32;
-        }
-        const int bAt = __shfl_sync(0xffffffffu, bv, rA & 31);
-        const int aAt = __shfl_sync(0xffffffffu, a, rB & 31);
-        const bool commonA = takeA && rA < 32 && bAt == a;
-        const bool commonB = takeB && rB < 32 && aAt == bv;
-        const uint32_t cmask = __ballot_sync(0xffffffffu, commonA);
-        if (takeA) {
-            const int pos = lane + rA - __popc(cmask & lt);
-            wl[base + out + pos] = (uint32_t)a | (1u << 30) | (commonA ? (1u << 31) : 0u);
-        }
-        if (takeB && !commonB) {
-            const uint32_t below = rB >= 32 ? 0xffffffffu : ((1u << rB) - 1u);
-            const int pos = lane + rB - __popc(cmask & below);
-            wl[base + out + pos] = (uint32_t)bv | (1u << 31);
-        }
-        const int nTA = __popc(__ballot_sync(0xffffffffu, takeA));
-        const int nTB = __popc(__ballot_sync(0xffffffffu, takeB));
-        out += nTA + nTB - __popc(cmask);
-        pa += nTA;
-        pb += nTB;
     }
-    if (lane == 0) wl_len[tile] = (int32_t)out;
+    if (lane == 31) {
+        sh[w] = inc.b;
+        sh[16 + w] = inc.o0;
+        sh[32 + w] = inc.o1;
+    }
+    __syncthreads();
+    if (w == 0) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            int x = lane < kWlThreads / 32 ? sh[16 * k + lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int n = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += n;
+            }
+            if (lane < kWlThreads / 32) sh[16 * k + lane] = x;
+        }
+    }
+    __syncthreads();
+    Seg3 ex;
+    ex.b = inc.b - v.b + (w ? sh[w - 1] : 0);
+    ex.o0 = inc.o0 - v.o0 + (w ? sh[16 + w - 1] : 0);
+    ex.o1 = inc.o1 - v.o1 + (w ? sh[32 + w - 1] : 0);
+    tot_out->b = sh[kWlThreads / 32 - 1];
+    tot_out->o0 = sh[16 + kWlThreads / 32 - 1];
+    tot_out->o1 = sh[32 + kWlThreads / 32 - 1];
+    __syncthreads();
+    return ex;
+}
+
+__global__ void __launch_bounds__(kWlThreads) worklist_kernel(const int64_t* __restrict__ offsets,
+                                                              const int32_t* __restrict__ indices,
+                                                              uint32_t* __restrict__ wl, int32_t* __restrict__ wl_len,
+                                                              int64_t BH, int64_t Np, int64_t n_it, int64_t N,
+                                                              int32_t pq, int32_t stripe_words) {
+    extern __shared__ uint32_t bm[];  // [4][stripe_words]
+    __shared__ int sh[48];
+    const int64_t item = blockIdx.x;
+    const int64_t bh = item / n_it, it = item % n_it;
+    const int G = 256 / pq;
+    const int64_t i0 = it * G;
+    const int nb = (int)min((int64_t)G, Np - i0);
+    const int64_t r0 = bh * Np + i0;
+    const int64_t out_base = offsets[r0];
+    const int tid = threadIdx.x;
+    const int stripe = stripe_words * 32;
+    const int n_stripes = (int)((N + stripe - 1) / stripe);
+    // tile 0 = blocks [0, G/2), tile 1 = blocks [G/2, G)
+    const uint32_t t0mask = G == 4 ? 0x3u : 0x1u;
+    Seg3 total = {0, 0, 0};   // segment lengths (pass 0 counts them when striped)
+    Seg3 run = {0, 0, 0};     // running output position per segment
+    for (int pass = (n_stripes > 1 ? 0 : 1); pass < 2; ++pass) {
+        run = {0, 0, 0};
+        for (int64_t ss = 0; ss < N; ss += stripe) {
+            const int words = (int)min((int64_t)stripe_words, (N - ss + 31) / 32);
+            for (int x = tid; x < 4 * stripe_words; x += kWlThreads) bm[x] = 0u;
+            __syncthreads();
+            for (int b = 0; b < nb; ++b) {
+                const int64_t a = offsets[r0 + b], e = offsets[r0 + b + 1];
+                for (int64_t t = a + tid; t < e; t += kWlThreads) {
+                    const int64_t key = indices[t];
+                    if (key >= ss && key < ss + stripe) {
+                        const int kk = (int)(key - ss);
+                        atomicOr(&bm[b * stripe_words + (kk >> 5)], 1u << (kk & 31));
+                    }
+                }
+            }
+            __syncthreads();
+            const int per = (words + kWlThreads - 1) / kWlThreads;
+            const int w0 = min(words, tid * per), w1 = min(words, w0 + per);
+            Seg3 cnt = {0, 0, 0};
+            for (int x = w0; x < w1; ++x) {
+                const uint32_t b0 = bm[x], b1 = bm[stripe_words + x], b2 = bm[2 * stripe_words + x],
+                               b3 = bm[3 * stripe_words + x];
+                const uint32_t u0 = t0mask == 0x3u ? (b0 | b1) : b0;
+                const uint32_t u1 = t0mask == 0x3u ? (b2 | b3) : b1;
+                cnt.b += __popc(u0 & u1);
+                cnt.o0 += __popc(u0 & ~u1);
+                cnt.o1 += __popc(u1 & ~u0);
+            }
+            Seg3 stot;
+            const Seg3 ex = block_scan3(cnt, &stot, sh);
+            if (pass == 1) {
+                const Seg3 seg_base = n_stripes > 1 ? total : stot;  // full segment lengths
+                int64_t pb = out_base + run.b + ex.b;
+                int64_t p0 = out_base + seg_base.b + run.o0 + ex.o0;
+                int64_t p1 = out_base + seg_base.b + seg_base.o0 + run.o1 + ex.o1;
+                for (int x = w0; x < w1; ++x) {
+                    const uint32_t b0 = bm[x], b1 = bm[stripe_words + x], b2 = bm[2 * stripe_words + x],
+                                   b3 = bm[3 * stripe_words + x];
+                    const uint32_t u0 = t0mask == 0x3u ? (b0 | b1) : b0;
+                    const uint32_t u1 = t0mask == 0x3u ? (b2 | b3) : b1;
+                    uint32_t u = u0 | u1;
+                    while (u) {
+                        const int bit = __ffs(u) - 1;
+                        const uint32_t m = 1u << bit;
+                        const uint32_t mem = ((b0 & m) ? 1u : 0u) | ((b1 & m) ? 2u : 0u) | ((b2 & m) ? 4u : 0u) |
+                                             ((b3 & m) ? 8u : 0u);
+                        const uint32_t e = (uint32_t)(ss + x * 32 + bit) | (mem << 28);
+                        if ((u0 & m) && (u1 & m)) wl[pb++] = e;
+                        else if (u0 & m) wl[p0++] = e;
+                        else wl[p1++] = e;
+                        u &= u - 1;
+                    }
+                }
+                if (n_stripes == 1) total = stot;
+            }
+            run.b += stot.b;
+            run.o0 += stot.o0;
+            run.o1 += stot.o1;
+            __syncthreads();
+        }
+        if (pass == 0) total = run;
+    }
+    if (tid == 0) {
+        wl_len[3 * item] = total.b;
+        wl_len[3 * item + 1] = total.o0;
+        wl_len[3 * item + 2] = total.o1;
+    }
 }
 
 cudaError_t launch_worklist(const int64_t* offsets, const int32_t* indices, uint32_t* wl, int32_t* wl_len,
-                            int64_t BH, int64_t Np, int64_t n_mt, int32_t pq, cudaStream_t st) {
-    const int64_t tiles = BH * n_mt;
-    const int64_t blocks = (tiles * 32 + 255) / 256;
-    if (blocks <= 0) return cudaSuccess;
-    worklist_kernel<<<(unsigned)blocks, 256, 0, st>>>(offsets, indices, wl, wl_len, BH, Np, n_mt, pq);
+                            int64_t BH, int64_t Np, int64_t n_it, int64_t N, int32_t pq, cudaStream_t st) {
+    const int64_t items = BH * n_it;
+    if (items <= 0) return cudaSuccess;
+    const int stripe_words = (int)min((int64_t)kStripeWords, (N + 31) / 32);
+    const int smem = 4 * stripe_words * 4;
+    cudaError_t e = cudaFuncSetAttribute(worklist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    worklist_kernel<<<(unsigned)items, kWlThreads, smem, st>>>(offsets, indices, wl, wl_len, BH, Np, n_it, N, pq,
+                                                               stripe_words);
     return cudaGetLastError();
 }
 
@@ -605,7 +827,7 @@ static cudaError_t launch_attn_t(const AttnParams& p, int grid, cudaStream_t st)
     auto kern = attn_kernel<D, GATHER>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, kAttnThreads, C::kSmem, st>>>(p);
+    kern<<<grid, kThreads, C::kSmem, st>>>(p);
     return cudaGetLastError();
 }
 

@@ -160,15 +160,19 @@ VA_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "
 // K-major SW128 (rows of 128 B, 8-row atoms of 1024 B): LBO unused (=16 B), SBO = 1024 B.
 // MN-major SW128 (128 B = 64 elements along MN, rows along K): LBO = byte stride between
 // 64-element MN blocks, SBO = byte stride between 8-row K groups (1024 B here).
-VA_DEV uint64_t make_sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+VA_DEV uint64_t make_sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout = 2u) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
     d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
     d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
-    d |= (uint64_t)1u << 46;  // version
-    d |= (uint64_t)2u << 61;  // SWIZZLE_128B
+    d |= (uint64_t)1u << 46;       // version
+    d |= (uint64_t)layout << 61;   // 2 = SWIZZLE_128B, 0 = SWIZZLE_NONE (interleaved core matrices)
     return d;
 }
+// K-major SWIZZLE_NONE layout of a [rows x 16] bf16 tile: 8x8 core matrices (128 B each),
+// element (r, e) at ((r/8)*2 + e/8)*128 + (r%8)*16 + (e%8)*2; K-direction core stride (LBO)
+// 128 B, 8-row-group stride (SBO) 256 B.
+VA_DEV uint32_t k16_offset(int r, int e) { return ((r >> 3) * 2 + (e >> 3)) * 128 + (r & 7) * 16 + (e & 7) * 2; }
 // Instruction descriptor, kind::f16 with bf16 A/B and f32 accumulate:
 //   [4,6) c_format=1 (F32)  [7,10) a_format=1 (BF16)  [10,13) b_format=1 (BF16)
 //   [15] a_major (0=K,1=MN) [16] b_major  [17,23) N>>3  [24,29) M>>4
@@ -186,6 +190,27 @@ VA_DEV float ex2(float x) {
 VA_DEV uint32_t pack_bf16x2(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&v);
+}
+// Packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 process two fp32 lanes per instruction).
+VA_DEV uint64_t pack_f32x2(float lo, float hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+VA_DEV float2 unpack_f32x2(uint64_t v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+VA_DEV uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+VA_DEV float2 fadd2(float2 a, float2 b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pack_f32x2(a.x, a.y)), "l"(pack_f32x2(b.x, b.y)));
+    return unpack_f32x2(d);
 }
 // Order-preserving map fp32 -> u32 (a < b  <=>  key(a) < key(b) for non-NaN).
 VA_DEV uint32_t f32_order_key(float f) {

@@ -8,6 +8,7 @@
 #include <cudaTypedefs.h>
 #include <math.h>
 #include <mutex>
+#include <stdlib.h>
 #include <string.h>
 
 namespace {
@@ -63,7 +64,7 @@ vecattn_status_t check_problem(const vecattn_problem_t* p) {
     if (!p) return VECATTN_ERR_INVALID_ARGUMENT;
     if (p->B < 1 || p->Hq < 1 || p->Hkv < 1 || p->N < 1) return VECATTN_ERR_SHAPE;
     if (p->D != 64 && p->D != 128) return VECATTN_ERR_SHAPE;
-    if (p->N >= (int64_t(1) << 30) || p->Hq > 1024) return VECATTN_ERR_SHAPE;
+    if (p->N >= (int64_t(1) << 28) || p->Hq > 1024) return VECATTN_ERR_SHAPE;
     if (p->B * p->Hkv * p->N >= (int64_t(1) << 31) || p->B * p->Hq * p->N >= (int64_t(1) << 31))
         return VECATTN_ERR_SHAPE;
     if (p->Hq % p->Hkv != 0) return VECATTN_ERR_INVALID_ARGUMENT;
@@ -186,9 +187,18 @@ vecattn_status_t set_k_map(const vecattn_problem_t* p, const void* k, int bn, Se
     return VECATTN_OK;
 }
 
-#define VA_CU(x)                                       \
-    do {                                               \
-        if ((x) != cudaSuccess) return VECATTN_ERR_CUDA; \
+thread_local cudaError_t g_last_cuda_error = cudaSuccess;
+
+vecattn_status_t cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return VECATTN_OK;
+    g_last_cuda_error = e;
+    return VECATTN_ERR_CUDA;
+}
+
+#define VA_CU(x)                                            \
+    do {                                                    \
+        cudaError_t e_ = (x);                               \
+        if (e_ != cudaSuccess) return cuda_status(e_);      \
     } while (0)
 
 __global__ void validate_kernel(const int64_t* __restrict__ offsets, const int32_t* __restrict__ indices,
@@ -213,6 +223,8 @@ __global__ void validate_kernel(const int64_t* __restrict__ offsets, const int32
 extern "C" {
 
 int32_t vecattn_abi_version(void) { return 1; }
+
+const char* vecattn_last_cuda_error(void) { return cudaGetErrorString(g_last_cuda_error); }
 
 const char* vecattn_status_string(vecattn_status_t s) {
     switch (s) {
@@ -283,7 +295,7 @@ vecattn_status_t vecattn_select(const vecattn_problem_t* p, const vecattn_select
         e = va::launch_emit(w.bitmask, sp->words_per_row, offsets, d_nnz, cap, indices, sp->BH, sp->Np, p->N,
                             s->pq, p->causal ? 1 : 0, cs);
     delete sp;
-    return e == cudaSuccess ? VECATTN_OK : VECATTN_ERR_CUDA;
+    return cuda_status(e);
 }
 
 vecattn_status_t vecattn_debug_scores(const vecattn_problem_t* p, int32_t pq, const void* q, const void* k,
@@ -309,13 +321,13 @@ vecattn_status_t vecattn_debug_scores(const vecattn_problem_t* p, int32_t pq, co
     cudaError_t e = va::launch_pool(q, w.qp, sp->BH, p->N, p->D, pq, cs);
     if (e == cudaSuccess) e = va::launch_select(*sp, va::EPI_SCORES, (int)p->D, cs);
     delete sp;
-    return e == cudaSuccess ? VECATTN_OK : VECATTN_ERR_CUDA;
+    return cuda_status(e);
 }
 
 size_t vecattn_sparse_workspace_bytes(const vecattn_problem_t* p, int32_t pq, int64_t nnz_cap) {
     if (check_problem(p) != VECATTN_OK || (pq != 64 && pq != 128) || nnz_cap < 0) return 0;
-    const int64_t n_mt = (p->N + 127) / 128;
-    return align_up((size_t)nnz_cap * 4) + align_up((size_t)(p->B * p->Hq * n_mt) * 4) + kAlign;
+    const int64_t n_it = (p->N + 255) / 256;
+    return align_up((size_t)nnz_cap * 4) + align_up((size_t)(p->B * p->Hq * n_it) * 12) + kAlign;
 }
 
 static vecattn_status_t attn_common(const vecattn_problem_t* p, const void* q, const void* k, const void* v,
@@ -331,7 +343,7 @@ static vecattn_status_t attn_common(const vecattn_problem_t* p, const void* q, c
     ap.BH = p->B * p->Hq;
     ap.Hq = p->Hq;
     ap.Hkv = p->Hkv;
-    ap.n_mt = (p->N + 127) / 128;
+    ap.n_mt = (p->N + 255) / 256;
     ap.total_items = ap.BH * ap.n_mt;
     ap.causal = p->causal ? 1 : 0;
     ap.scale = scale;
@@ -367,7 +379,7 @@ vecattn_status_t vecattn_sparse_fwd(const vecattn_problem_t* p, int32_t pq, cons
     uint8_t* b = static_cast<uint8_t*>(ws);
     uint32_t* wl = reinterpret_cast<uint32_t*>(b);
     int32_t* wl_len = reinterpret_cast<int32_t*>(b + align_up((size_t)nnz_cap * 4));
-    int* counter = reinterpret_cast<int*>(b + align_up((size_t)nnz_cap * 4) + align_up((size_t)(ap->BH * ap->n_mt) * 4));
+    int* counter = reinterpret_cast<int*>(b + align_up((size_t)nnz_cap * 4) + align_up((size_t)(ap->BH * ap->n_mt) * 12));
     ap->Np = n_pooled(p, pq);
     ap->pq = pq;
     ap->wl = wl;
@@ -375,11 +387,11 @@ vecattn_status_t vecattn_sparse_fwd(const vecattn_problem_t* p, int32_t pq, cons
     ap->wl_len = wl_len;
     ap->work_counter = counter;
     cudaError_t e = va::launch_worklist(offsets, indices ? indices : reinterpret_cast<const int32_t*>(wl), wl, wl_len,
-                                        ap->BH, ap->Np, ap->n_mt, pq, cs);
+                                        ap->BH, ap->Np, ap->n_mt, p->N, pq, cs);
     if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, sizeof(int), cs);
     if (e == cudaSuccess) e = va::launch_attn(*ap, (int)p->D, true, attn_grid(ap->total_items), cs);
     delete ap;
-    return e == cudaSuccess ? VECATTN_OK : VECATTN_ERR_CUDA;
+    return cuda_status(e);
 }
 
 size_t vecattn_dense_workspace_bytes(const vecattn_problem_t* p) {
@@ -402,13 +414,13 @@ vecattn_status_t vecattn_dense_fwd(const vecattn_problem_t* p, const void* q, co
          !tmap_3d(&ap->tm_v, v, (uint64_t)p->D, (uint64_t)p->N, (uint64_t)(p->B * p->Hkv), 128)))
         st = VECATTN_ERR_UNSUPPORTED;
     if (st != VECATTN_OK) { delete ap; return st; }
-    ap->Np = ap->n_mt;
+    ap->Np = (p->N + 127) / 128;
     ap->pq = 128;
     ap->work_counter = reinterpret_cast<int*>(ws);
     cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(int), cs);
     if (e == cudaSuccess) e = va::launch_attn(*ap, (int)p->D, false, attn_grid(ap->total_items), cs);
     delete ap;
-    return e == cudaSuccess ? VECATTN_OK : VECATTN_ERR_CUDA;
+    return cuda_status(e);
 }
 
 vecattn_status_t vecattn_validate_selection(const vecattn_problem_t* p, int32_t pq, const int64_t* offsets,

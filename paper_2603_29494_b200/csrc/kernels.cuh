@@ -68,17 +68,17 @@ struct AttnParams {
     const __nv_bfloat16* v;
     __nv_bfloat16* o;              // [B*Hq, N, D]
     float* lse;                    // [B*Hq, N] or null
-    const uint32_t* wl;            // gather: union entries (key | inA<<30 | inB<<31)
-    const int64_t* offsets;        // gather: CSR offsets [B*Hq*Np + 1] (pair base = offsets[bh*Np + G*pair])
-    const int32_t* wl_len;         // gather: [B*Hq*n_mt] union length per 128-row tile
+    const uint32_t* wl;            // gather: union entries (key | membership bits << 28, bit b = block b of the item)
+    const int64_t* offsets;        // gather: CSR offsets [B*Hq*Np + 1] (item base = offsets[bh*Np + (256/pq)*item])
+    const int32_t* wl_len;         // gather: [B*Hq*n_mt][3] union segment lengths (both tiles | tile 0 | tile 1)
     int* work_counter;             // dynamic tile scheduler (zeroed before launch)
-    int64_t N, Np, BH, Hq, Hkv, n_mt, total_items;
+    int64_t N, Np, BH, Hq, Hkv, n_mt /* 256-row items per head */, total_items;
     int32_t pq, causal;
     float scale, scale_log2;
 };
 
 cudaError_t launch_worklist(const int64_t* offsets, const int32_t* indices, uint32_t* wl, int32_t* wl_len,
-                            int64_t BH, int64_t Np, int64_t n_mt, int32_t pq, cudaStream_t st);
+                            int64_t BH, int64_t Np, int64_t n_it, int64_t N, int32_t pq, cudaStream_t st);
 cudaError_t launch_attn(const AttnParams& p, int D, bool gather, int grid, cudaStream_t st);
 
 }  // namespace va

@@ -66,6 +66,7 @@ def load(path: str = LIB_PATH):
         "vecattn_validate_selection": (i32, [prob, i32, vp, vp, vp, vp]),
         "vecattn_debug_scores": (i32, [prob, i32, vp, vp, vp, vp, sz, vp]),
         "vecattn_status_string": (ctypes.c_char_p, [i32]),
+        "vecattn_last_cuda_error": (ctypes.c_char_p, []),
         "vecattn_abi_version": (i32, []),
     }
     for name, (res, args) in sig.items():
@@ -78,7 +79,8 @@ def load(path: str = LIB_PATH):
 
 EXPORTED = ["vecattn_pool", "vecattn_select_workspace_bytes", "vecattn_select", "vecattn_sparse_workspace_bytes",
             "vecattn_sparse_fwd", "vecattn_dense_workspace_bytes", "vecattn_dense_fwd",
-            "vecattn_validate_selection", "vecattn_debug_scores", "vecattn_status_string", "vecattn_abi_version"]
+            "vecattn_validate_selection", "vecattn_debug_scores", "vecattn_status_string", "vecattn_last_cuda_error",
+            "vecattn_abi_version"]
 
 
 def _ptr(t):
@@ -92,7 +94,10 @@ def _stream(stream=None):
 
 def _check(fn, rc):
     if rc != 0:
-        raise VecAttnError(fn, rc)
+        err = VecAttnError(fn, rc)
+        if rc == 5:
+            err.args = (f"{err.args[0]}: {load().vecattn_last_cuda_error().decode()}",)
+        raise err
 
 
 def _dev_check(*ts):
