@@ -117,6 +117,25 @@ VECATTN_API vecattn_status_t vecattn_sparse_fwd(const vecattn_problem_t* p, int3
                                     int64_t nnz_cap, void* o, float* lse, void* ws, size_t ws_bytes,
                                     vecattn_stream_t stream);
 
+/* ------------------------------------------------------- fused stage 1+2 */
+
+VECATTN_API size_t vecattn_forward_workspace_bytes(const vecattn_problem_t* p, const vecattn_select_params_t* s,
+                                                   int64_t nnz_cap);
+
+/* The whole hot path in one call: selection (as vecattn_select) followed by
+ * vector-sparse attention (as vecattn_sparse_fwd) over that selection, without the
+ * CSR round trip -- the attention plan (per 256-row item: the union of its blocks'
+ * selections with per-block membership) is built directly from the on-chip-produced
+ * selection bitmask.  `offsets` and `*d_nnz` are always written; `indices` (CSR, may
+ * be NULL with cap = 0) is written iff nnz <= cap.  The attention runs iff
+ * nnz <= nnz_cap (the workspace's plan capacity); otherwise o/lse are untouched and the
+ * caller reads d_nnz, grows the workspace and calls again.                          */
+VECATTN_API vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_select_params_t* s,
+                                             const void* q, const void* k, const void* v, int64_t* offsets,
+                                             int32_t* indices, int64_t cap, int64_t* d_nnz, int64_t nnz_cap,
+                                             void* o, float* lse, void* ws, size_t ws_bytes,
+                                             vecattn_stream_t stream);
+
 /* ------------------------------------------------------------- reference */
 
 VECATTN_API size_t vecattn_dense_workspace_bytes(const vecattn_problem_t* p);

@@ -7,24 +7,24 @@
 // rows (Alg. 2; App. D.2).
 //
 // B200 design (DESIGN.md §6 "attn_kernel"):
-//  * Work item = 256 query rows = two M=128 tcgen05 tiles sharing every K/V chunk,
-//    so each gathered K/V row feeds 256 query rows (halves gather bytes per flop vs
-//    a single 128-row tile).  The paper's query block is P_q = 64 rows (P:335,
-//    P:690-696): an item covers 256/P_q adjacent blocks and iterates over the sorted
-//    UNION of their index lists (worklist_kernel).  Each union entry carries one
-//    membership bit per block; keys outside a row's own Idx(i) get score -inf, so
-//    every row computes exactly Eq. 5 for its own block.
-//  * K/V rows are gathered with TMA tile::gather4 (4 rows x 128 B per instruction)
-//    into 128B-swizzled shared memory by 4 loader warps (32 keys each, union entries
-//    prefetched one chunk ahead), 128 keys per chunk.
-//  * MMA warp, FA4-style ping-pong between the two tiles: S_t = Q_t K^T (M=N=128,
-//    K=D) into TMEM; P_t (bf16, written by softmax warpgroup t over S_t) feeds
-//    O_t += P_t V with A = P from TMEM and B = V (MN-major) from shared memory.
-//    Tensor order per chunk: PV0(c), S0(c+1), PV1(c), S1(c+1) -- while one
-//    warpgroup computes its softmax the tensor core works for the other.
-//  * Softmax warpgroup t: thread = query row = TMEM lane; masked row max in a
-//    first TMEM pass, lazy rescale (threshold 2^8, warp-voted because tcgen05.ld/st
-//    are warp-collective), exp2 with f32x2 FMA/ADD in a second pass.
+//  * Work item = 256 query rows = two M=128 tcgen05 tiles sharing every K/V chunk.
+//    The paper's query block is P_q = 64 rows: an item covers
+//    256/P_q adjacent blocks.  Its key plan (worklist_kernel / plan_kernel) is the
+//    union of their index lists, one membership bit per block (entry = key | bits<<28),
+//    in three sorted segments: keys used by both tiles (gathered once, computed by
+//    both), by tile 0 only, by tile 1 only.  Softmax is order-invariant, so each row
+//    still computes exactly Eq. 5 over its own Idx(i).
+//  * Membership masking runs on the tensor core: S = [Q | onehot(block)] [K | bias]^T
+//    with one extra K=16 MMA step, bias = 0 (member) or -2^100 (non-member).
+//  * 64-key chunks, 4-stage K and V rings; K/V rows gathered with TMA tile::gather4
+//    (4 rows x 128 B per instruction) by 2 K-loader and 2 V-loader warps (32 keys
+//    each, plan entries prefetched one chunk ahead); dense mode uses 64x64 TMA tiles.
+//  * MMA warp: S_t = Q_t K^T (M=128, N=64) into double-buffered TMEM per tile, issued
+//    one chunk ahead; O_t += P_t V with A = P_t from TMEM (bf16, written by the softmax
+//    over S_t) and B = V (MN-major) from shared memory.
+//  * Softmax warpgroup t (thread = query row = TMEM lane): row max in a first TMEM
+//    pass, lazy rescale (threshold 2^8, warp-voted because tcgen05.ld/st are
+//    warp-collective), exp2 with f32x2 FMA/ADD in a second pass.
 //  * Persistent CTAs, dynamic atomic scheduler, items head-major (one head's K/V
 //    stays L2-resident), causal items longest-first.
 // Degenerate rows (no visible selected key; reading R6): O_r = V_r,
@@ -42,46 +42,50 @@ constexpr int kThreads = 448;  // w0 sched+Q, w1 MMA, w2-5 softmax tile 0, w6-9 
 constexpr int kLoadWarps = 4;
 constexpr int kFirstLoadWarp = 10;
 constexpr int kSoftmaxThreads = 256;
+constexpr int kChunk = 64;                  // keys per K/V chunk
 constexpr uint32_t kKeyMask = 0x0FFFFFFFu;  // entry = key | membership << 28
 constexpr uint32_t kPad = 0x0FFFFFFFu;      // meta key for padding lanes (sorts last)
 
 template <int D>
 struct AttnCfg {
-    static constexpr int kStages = D == 128 ? 2 : 4;
+    static constexpr int kStages = D == 128 ? 4 : 8;
     static constexpr int kCB = D / 64;
-    static constexpr int kTileBytes = kCB * 128 * 128;  // 128 rows x D bf16
-    static constexpr int kOffQ = 0;                      // two Q tiles
-    static constexpr int kOffK = 2 * kTileBytes;
-    static constexpr int kOffV = kOffK + kStages * kTileBytes;
-    static constexpr int kOffMeta = kOffV + kStages * kTileBytes;
-    static constexpr int kMetaWords = 128;               // keys[128] (causal prefix search)
-    static constexpr int kOffQx = (kOffMeta + kStages * kMetaWords * 4 + 1023) / 1024 * 1024;  // Q_ext [2][128 x 16] bf16
-    static constexpr int kOffKx = kOffQx + 2 * 128 * 16 * 2;               // K_ext [stages][128 x 16] bf16
-    static constexpr int kOffBar = kOffKx + kStages * 128 * 16 * 2;
+    static constexpr int kQTileBytes = kCB * 128 * 128;   // 128 rows x D bf16
+    static constexpr int kKVBytes = kCB * kChunk * 128;    // 64 keys x D bf16
+    static constexpr int kOffQ = 0;                        // two Q tiles
+    static constexpr int kOffK = 2 * kQTileBytes;
+    static constexpr int kOffV = kOffK + kStages * kKVBytes;
+    static constexpr int kOffMeta = kOffV + kStages * kKVBytes;
+    static constexpr int kOffQx = (kOffMeta + kStages * kChunk * 4 + 1023) / 1024 * 1024;  // Q_ext [2][128 x 16]
+    static constexpr int kOffKx = kOffQx + 2 * 128 * 16 * 2;                               // K_ext [S][64 x 16]
+    static constexpr int kOffBar = kOffKx + kStages * kChunk * 16 * 2;
     static constexpr int B_QFULL = 0, B_QEMPTY = 1, B_KFULL = 2, B_KEMPTY = B_KFULL + kStages,
                          B_VFULL = B_KEMPTY + kStages, B_VEMPTY = B_VFULL + kStages,
-                         B_MFULL = B_VEMPTY + kStages, B_SFULL = B_MFULL + kStages, B_PFULL = B_SFULL + 2,
-                         B_ODONE = B_PFULL + 2, B_OEMPTY = B_ODONE + 2, B_IFULL = B_OEMPTY + 2,
-                         B_IEMPTY = B_IFULL + 2, kNumBars = B_IEMPTY + 2;
+                         B_MFULL = B_VEMPTY + kStages, B_SFULL = B_MFULL + kStages /* [2 tiles][2 bufs] */,
+                         B_PFULL = B_SFULL + 4, B_ODONE = B_PFULL + 4, B_OEMPTY = B_ODONE + 2,
+                         B_IFULL = B_OEMPTY + 2, B_IEMPTY = B_IFULL + 2, kNumBars = B_IEMPTY + 2;
     static constexpr int kOffItem = kOffBar + kNumBars * 8;
     static constexpr int kSmem = kOffItem + 16;
-    static constexpr uint32_t kTmemCols = 512;  // tile t: S_t [256t, 256t+128) (P_t over its first 64), O_t [256t+128, ...)
-    static constexpr uint32_t kIdescS = make_idesc_bf16(128, 128, 0, 0);
+    // TMEM: O_t at 128t (D cols); S[t][b] at 256 + 128t + 64b (64 cols; P over its first 32)
+    static constexpr uint32_t kTmemCols = 512;
+    static constexpr uint32_t kIdescS = make_idesc_bf16(128, kChunk, 0, 0);
     static constexpr uint32_t kIdescPV = make_idesc_bf16(128, D, 0, 1);
 };
+
+VA_DEV uint32_t s_col(int t, int b) { return 256u + 128u * t + 64u * b; }
 
 struct Item {
     int64_t bh, it;  // head, 256-row item within the head
     int n_chunks;
-    int lb, l0, l1;  // gather: union segment lengths (keys of both tiles | tile 0 only | tile 1 only)
+    int lb, l0, l1;  // gather: plan segment lengths (keys of both tiles | tile 0 only | tile 1 only)
     int nb, n0, n1;  // gather: chunks per segment
     int len;         // dense: key extent
-    int64_t base;    // gather: worklist base
+    int64_t base;    // gather: plan base
 };
 
 struct Chunk {
     int mask;   // bit t: tile t computes this chunk
-    int start;  // first worklist entry (relative to the item base) / first key (dense)
+    int start;  // first plan entry (relative to the item base) / first key (dense)
     int len;    // valid entries / keys
 };
 
@@ -96,9 +100,9 @@ VA_DEV Item decode_item(const AttnParams& p, int item) {
         I.lb = p.wl_len[3 * x];
         I.l0 = p.wl_len[3 * x + 1];
         I.l1 = p.wl_len[3 * x + 2];
-        I.nb = (I.lb + 127) / 128;
-        I.n0 = (I.l0 + 127) / 128;
-        I.n1 = (I.l1 + 127) / 128;
+        I.nb = (I.lb + kChunk - 1) / kChunk;
+        I.n0 = (I.l0 + kChunk - 1) / kChunk;
+        I.n1 = (I.l1 + kChunk - 1) / kChunk;
         I.n_chunks = I.nb + I.n0 + I.n1;
         I.base = p.offsets[I.bh * p.Np + G * I.it];
         I.len = 0;
@@ -106,7 +110,7 @@ VA_DEV Item decode_item(const AttnParams& p, int item) {
         const int64_t kend = p.causal ? min(p.N, (I.it + 1) * 256) : p.N;
         I.len = (int)kend;
         I.base = 0;
-        I.n_chunks = (int)((kend + 127) / 128);
+        I.n_chunks = (int)((kend + kChunk - 1) / kChunk);
         I.lb = I.l0 = I.l1 = I.nb = I.n0 = I.n1 = 0;
     }
     return I;
@@ -119,14 +123,14 @@ VA_DEV Chunk chunk_info(const Item& I, int j) {
     Chunk c;
     if constexpr (!GATHER) {
         c.mask = 3;
-        c.start = 128 * j;
-        c.len = min(128, I.len - 128 * j);
+        c.start = kChunk * j;
+        c.len = min(kChunk, I.len - kChunk * j);
         return c;
     } else {
         if (j < I.nb) {
             c.mask = 3;
-            c.start = 128 * j;
-            c.len = min(128, I.lb - 128 * j);
+            c.start = kChunk * j;
+            c.len = min(kChunk, I.lb - kChunk * j);
             return c;
         }
         const int k = j - I.nb;
@@ -141,11 +145,11 @@ VA_DEV Chunk chunk_info(const Item& I, int j) {
         }
         c.mask = 1 << t;
         if (t == 0) {
-            c.start = I.lb + 128 * q;
-            c.len = min(128, I.l0 - 128 * q);
+            c.start = I.lb + kChunk * q;
+            c.len = min(kChunk, I.l0 - kChunk * q);
         } else {
-            c.start = I.lb + I.l0 + 128 * q;
-            c.len = min(128, I.l1 - 128 * q);
+            c.start = I.lb + I.l0 + kChunk * q;
+            c.len = min(kChunk, I.l1 - kChunk * q);
         }
         return c;
     }
@@ -170,6 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
+    if (p.d_nnz != nullptr && *p.d_nnz > p.nnz_cap) return;  // fused path: plan not built (capacity)
 
     if (threadIdx.x == 0) {
         if ((smem_u32(smem) & 1023u) != 0) __trap();
@@ -182,9 +187,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             mbar_init(&bars[C::B_VEMPTY + s], 1);
             mbar_init(&bars[C::B_MFULL + s], 2);
         }
+        for (int x = 0; x < 4; ++x) {
+            mbar_init(&bars[C::B_SFULL + x], 1);
+            mbar_init(&bars[C::B_PFULL + x], 128);
+        }
         for (int t = 0; t < 2; ++t) {
-            mbar_init(&bars[C::B_SFULL + t], 1);
-            mbar_init(&bars[C::B_PFULL + t], 128);
             mbar_init(&bars[C::B_ODONE + t], 1);
             mbar_init(&bars[C::B_OEMPTY + t], 128);
             mbar_init(&bars[C::B_IFULL + t], 1);
@@ -195,8 +202,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     if constexpr (GATHER) {
         // Membership masking on the tensor core: S = [Q | E] [K | F]^T with E = one-hot of the
         // row's block (Q_ext, constant per row position) and F[j][b] = 0 if key j is in block
-        // b's index set else -2^100 (K_ext, written per chunk by the loaders).  Members get +0
-        // exactly; non-members a score of -2^100 whose exp2 underflows to 0.
+        // b's index set else -2^100 (K_ext, written per chunk by the K loaders).  Members get
+        // +0 exactly; non-members a score of -2^100 whose exp2 underflows to 0.
         uint16_t* qx = reinterpret_cast<uint16_t*>(smem + C::kOffQx);
         for (int x = threadIdx.x; x < 2 * 128 * 16; x += kThreads) {
             const int t = x / (128 * 16), r = (x / 16) % 128, e = x % 16;
@@ -204,7 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             qx[(t * 128 * 16 * 2 + k16_offset(r, e)) / 2] = (e == blk) ? 0x3F80u : 0u;  // bf16 1.0
         }
         uint32_t* kx = reinterpret_cast<uint32_t*>(smem + C::kOffKx);
-        for (int x = threadIdx.x; x < S_ * 128 * 16 / 2; x += kThreads) kx[x] = 0u;
+        for (int x = threadIdx.x; x < S_ * kChunk * 16 / 2; x += kThreads) kx[x] = 0u;
         fence_proxy_async();
     }
     if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -236,24 +243,23 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             if (I.n_chunks == 0) continue;
             if (lane == 0) {
                 if (qi > 0) mbar_wait(&bars[C::B_QEMPTY], (qi - 1) & 1);
-                mbar_arrive_expect_tx(&bars[C::B_QFULL], 2 * C::kTileBytes);
+                mbar_arrive_expect_tx(&bars[C::B_QFULL], 2 * C::kQTileBytes);
 #pragma unroll
                 for (int t = 0; t < 2; ++t)
 #pragma unroll
                     for (int cb = 0; cb < C::kCB; ++cb)
-                        tma_load_3d(sQ + t * C::kTileBytes + cb * 128 * 128, &p.tm_q, &bars[C::B_QFULL], cb * 64,
+                        tma_load_3d(sQ + t * C::kQTileBytes + cb * 128 * 128, &p.tm_q, &bars[C::B_QFULL], cb * 64,
                                     (int)(I.it * 256 + t * 128), (int)I.bh);
             }
             ++qi;
         }
     } else if (warp >= kFirstLoadWarp) {
         // ======================================== K/V loaders (4 warps)
-        // Warps 10-11 load K, warps 12-13 load V; warp (g & 1) owns chunk columns
-        // [64*(g&1), +64).  GATHER: each lane holds 2 union entries (prefetched one chunk
-        // ahead) and each warp issues 16 tile::gather4 per 128-B column block.  K loaders
-        // also write the K_ext membership-bias rows (consumed by the S MMA, freed with
-        // KEMPTY); V loaders publish the keys for the causal mask (freed with VEMPTY).
-        // K and V are decoupled so the K ring refills as soon as the S MMAs release it.
+        // Warps 10-11 load K, 12-13 load V; warp (g & 1) owns chunk columns [32*(g&1), +32).
+        // GATHER: one plan entry per lane (prefetched one chunk ahead); lanes 0-7 issue one
+        // tile::gather4 per 128-B column block.  K loaders also write the K_ext bias rows
+        // (consumed by the S MMA, freed with KEMPTY); V loaders publish the keys for the
+        // causal mask (freed with VEMPTY).  K and V rings are decoupled.
         const int g = (int)warp - kFirstLoadWarp;
         const bool isK = g < 2;
         const int sub = g & 1;
@@ -275,65 +281,49 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             const int64_t bh_kv = b * p.Hkv + h / (p.Hq / p.Hkv);
             if constexpr (GATHER) {
                 const uint32_t* wlp = p.wl + I.base;
-                const int col0 = 64 * sub + (int)lane, col1 = col0 + 32;
+                const int col = 32 * sub + (int)lane;
                 Chunk ch = chunk_info<true>(I, 0);
-                uint32_t e0 = col0 < ch.len ? __ldg(wlp + ch.start + col0) : 0u;
-                uint32_t e1 = col1 < ch.len ? __ldg(wlp + ch.start + col1) : 0u;
+                uint32_t e = col < ch.len ? __ldg(wlp + ch.start + col) : 0u;
                 for (int j = 0; j < I.n_chunks; ++j, ++c) {
                     const int s = (int)(c % S_);
                     const int round = (int)(c / S_);
-                    const bool ok0 = col0 < ch.len, ok1 = col1 < ch.len;
+                    const bool ok = col < ch.len;
                     Chunk chn;
                     chn.len = 0;
                     chn.start = 0;
                     if (j + 1 < I.n_chunks) chn = chunk_info<true>(I, j + 1);
-                    const uint32_t n0 = col0 < chn.len ? __ldg(wlp + chn.start + col0) : 0u;
-                    const uint32_t n1 = col1 < chn.len ? __ldg(wlp + chn.start + col1) : 0u;
-                    const uint32_t key0 = e0 & kKeyMask, key1 = e1 & kKeyMask;
-                    const int row0 = (int)(bh_kv * p.N + (ok0 ? key0 : 0u));
-                    const int row1 = (int)(bh_kv * p.N + (ok1 ? key1 : 0u));
+                    const uint32_t en = col < chn.len ? __ldg(wlp + chn.start + col) : 0u;
+                    const uint32_t key = e & kKeyMask;
+                    const int row = (int)(bh_kv * p.N + (ok ? key : 0u));
                     if (lane == 0 && round > 0) mbar_wait(&bars[bempty + s], (round - 1) & 1);
                     __syncwarp();
                     if (isK) {
-                        // K_ext rows: bias 0 for member blocks, -2^100 (bf16 0xF180) otherwise
-#pragma unroll
-                        for (int u = 0; u < 2; ++u) {
-                            const int kk = u ? col1 : col0;
-                            const uint32_t mem = (u ? ok1 : ok0) ? ((u ? e1 : e0) >> 28) : 0u;
-                            const uint32_t b0 = (mem & 1u) ? 0u : 0xF180u, b1 = (mem & 2u) ? 0u : 0xF180u;
-                            const uint32_t b2 = (mem & 4u) ? 0u : 0xF180u, b3 = (mem & 8u) ? 0u : 0xF180u;
-                            *reinterpret_cast<uint4*>(smem + C::kOffKx + s * 128 * 16 * 2 + k16_offset(kk, 0)) =
-                                make_uint4(b0 | (b1 << 16), b2 | (b3 << 16), 0u, 0u);
-                        }
-                        fence_proxy_async();  // generic-proxy smem writes -> tcgen05.mma (async proxy)
+                        // K_ext row: bias 0 for member blocks, -2^100 (bf16 0xF180) otherwise
+                        const uint32_t mem = ok ? (e >> 28) : 0u;
+                        const uint32_t b0 = (mem & 1u) ? 0u : 0xF180u, b1 = (mem & 2u) ? 0u : 0xF180u;
+                        const uint32_t b2 = (mem & 4u) ? 0u : 0xF180u, b3 = (mem & 8u) ? 0u : 0xF180u;
+                        *reinterpret_cast<uint4*>(smem + C::kOffKx + s * kChunk * 16 * 2 + k16_offset(col, 0)) =
+                            make_uint4(b0 | (b1 << 16), b2 | (b3 << 16), 0u, 0u);
+                        fence_proxy_async();  // generic-proxy smem write -> tcgen05.mma (async proxy)
                     } else {
-                        uint32_t* meta = sMeta + s * C::kMetaWords;
-                        meta[col0] = ok0 ? key0 : kPad;
-                        meta[col1] = ok1 ? key1 : kPad;
+                        sMeta[s * kChunk + col] = ok ? key : kPad;
                     }
                     __syncwarp();
                     if (lane == 0) {
                         if (!isK) mbar_arrive(&bars[C::B_MFULL + s]);
-                        mbar_arrive_expect_tx(&bars[bfull + s], 64 * D * 2);
+                        mbar_arrive_expect_tx(&bars[bfull + s], 32 * D * 2);
                     }
-                    // lane L < 16 gathers keys 4L..4L+3 of this warp's 64 (entries 0-31 in e0 of
-                    // lanes 0-31, 32-63 in e1)
                     const int q0 = (4 * (int)lane) & 31;
-                    const int ra = __shfl_sync(0xffffffffu, row0, q0), rb = __shfl_sync(0xffffffffu, row0, q0 + 1);
-                    const int rc = __shfl_sync(0xffffffffu, row0, q0 + 2), rd = __shfl_sync(0xffffffffu, row0, q0 + 3);
-                    const int sa = __shfl_sync(0xffffffffu, row1, q0), sb = __shfl_sync(0xffffffffu, row1, q0 + 1);
-                    const int sc = __shfl_sync(0xffffffffu, row1, q0 + 2), sd = __shfl_sync(0xffffffffu, row1, q0 + 3);
+                    const int ra = __shfl_sync(0xffffffffu, row, q0), rb = __shfl_sync(0xffffffffu, row, q0 + 1);
+                    const int rc = __shfl_sync(0xffffffffu, row, q0 + 2), rd = __shfl_sync(0xffffffffu, row, q0 + 3);
                     __syncwarp();
-                    if (lane < 16) {
-                        const bool hi = lane >= 8;
-                        uint8_t* dst = ring + s * C::kTileBytes + (64 * sub + 4 * (int)lane) * 128;
+                    if (lane < 8) {
+                        uint8_t* dst = ring + s * C::kKVBytes + (32 * sub + 4 * (int)lane) * 128;
 #pragma unroll
                         for (int cb = 0; cb < C::kCB; ++cb)
-                            tma_gather4(dst + cb * 128 * 128, tmap, &bars[bfull + s], cb * 64, hi ? sa : ra,
-                                        hi ? sb : rb, hi ? sc : rc, hi ? sd : rd);
+                            tma_gather4(dst + cb * kChunk * 128, tmap, &bars[bfull + s], cb * 64, ra, rb, rc, rd);
                     }
-                    e0 = n0;
-                    e1 = n1;
+                    e = en;
                     ch = chn;
                 }
             } else {
@@ -342,61 +332,65 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     const int s = (int)(c % S_);
                     const int round = (int)(c / S_);
                     if (round > 0) mbar_wait(&bars[bempty + s], (round - 1) & 1);
-                    uint8_t* dst = ring + s * C::kTileBytes;
-                    mbar_arrive_expect_tx(&bars[bfull + s], C::kTileBytes);
+                    uint8_t* dst = ring + s * C::kKVBytes;
+                    mbar_arrive_expect_tx(&bars[bfull + s], C::kKVBytes);
 #pragma unroll
                     for (int cb = 0; cb < C::kCB; ++cb)
-                        tma_load_3d(dst + cb * 128 * 128, tmap, &bars[bfull + s], cb * 64, j * 128, (int)bh_kv);
+                        tma_load_3d(dst + cb * kChunk * 128, tmap, &bars[bfull + s], cb * 64, j * kChunk,
+                                    (int)bh_kv);
                 }
                 __syncwarp();
             }
         }
     } else if (warp == 1) {
         // ======================================== MMA issuer (single thread)
-        // Per chunk c with tile mask m (next chunk mask mn):
-        //   S_t(c+1) for tiles entering at c+1 (early, overlaps softmax of c),
-        //   then for t in m: PV_t(c), S_t(c+1) if t continues.
+        // Per chunk c: S_t(c+1) for the tiles of chunk c+1 (double-buffered S, so it can run
+        // ahead of the softmax of c), then PV_t(c) for the tiles of chunk c.
         if (elect_one()) {
-            int64_t c = 0;            // global chunk counter (stage ring)
-            uint32_t cnt[2] = {0, 0}; // per-tile chunk counters (SFULL/PFULL/ODONE phases)
+            int64_t c = 0;                 // global chunk counter (stage rings)
+            uint32_t ns[2] = {0, 0};       // S issued per tile (buffer = ns & 1)
+            uint32_t np_[2] = {0, 0};      // PV issued per tile
             int qi = 0, oi = 0;
             const uint32_t qa = smem_u32(sQ);
+            auto wait_k = [&](int64_t cc) {
+                mbar_wait(&bars[C::B_KFULL + (int)(cc % S_)], (uint32_t)((cc / S_) & 1));
+                tc_fence_after();
+            };
             auto issue_s = [&](int t, int64_t cc) {
                 const int s = (int)(cc % S_);
-                const uint32_t ka = smem_u32(sK + s * C::kTileBytes);
-                const uint32_t q_t = qa + t * C::kTileBytes;
-                const uint32_t st = tmem_base + (uint32_t)(256 * t);
+                const int bi = (int)(ns[t] & 1u);
+                const uint32_t ka = smem_u32(sK + s * C::kKVBytes);
+                const uint32_t q_t = qa + t * C::kQTileBytes;
+                const uint32_t st = tmem_base + s_col(t, bi);
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                     const uint64_t adesc = make_sdesc(q_t + (kk >> 2) * 128 * 128 + (kk & 3) * 32, 16, 1024);
-                    const uint64_t bdesc = make_sdesc(ka + (kk >> 2) * 128 * 128 + (kk & 3) * 32, 16, 1024);
+                    const uint64_t bdesc = make_sdesc(ka + (kk >> 2) * kChunk * 128 + (kk & 3) * 32, 16, 1024);
                     mma_bf16_ss(st, adesc, bdesc, C::kIdescS, kk > 0 ? 1u : 0u);
                 }
                 if constexpr (GATHER) {  // + onehot(block) . bias(key, block)^T (membership mask)
                     const uint64_t adesc = make_sdesc(smem_u32(smem + C::kOffQx + t * 128 * 16 * 2), 128, 256, 0);
-                    const uint64_t bdesc = make_sdesc(smem_u32(smem + C::kOffKx + s * 128 * 16 * 2), 128, 256, 0);
+                    const uint64_t bdesc = make_sdesc(smem_u32(smem + C::kOffKx + s * kChunk * 16 * 2), 128, 256, 0);
                     mma_bf16_ss(st, adesc, bdesc, C::kIdescS, 1u);
                 }
-                mma_commit(&bars[C::B_SFULL + t]);
+                mma_commit(&bars[C::B_SFULL + 2 * t + bi]);
+                ++ns[t];
             };
             auto issue_pv = [&](int t, int64_t cc, bool first) {
                 const int s = (int)(cc % S_);
-                mbar_wait(&bars[C::B_PFULL + t], cnt[t] & 1u);
-                ++cnt[t];
+                const int bi = (int)(np_[t] & 1u);
+                mbar_wait(&bars[C::B_PFULL + 2 * t + bi], (np_[t] >> 1) & 1u);
+                ++np_[t];
                 tc_fence_after();
-                const uint32_t pt = tmem_base + (uint32_t)(256 * t);
-                const uint32_t ot = tmem_base + (uint32_t)(256 * t + 128);
-                const uint32_t va = smem_u32(sV + s * C::kTileBytes);
+                const uint32_t pt = tmem_base + s_col(t, bi);
+                const uint32_t ot = tmem_base + 128u * t;
+                const uint32_t va = smem_u32(sV + s * C::kKVBytes);
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint64_t bdesc = make_sdesc(va + kk * 16 * 128, 128 * 128, 1024);
+                for (int kk = 0; kk < kChunk / 16; ++kk) {
+                    const uint64_t bdesc = make_sdesc(va + kk * 16 * 128, kChunk * 128, 1024);
                     mma_bf16_ts(ot, pt + kk * 8, bdesc, C::kIdescPV, (first && kk == 0) ? 0u : 1u);
                 }
                 mma_commit(&bars[C::B_ODONE + t]);
-            };
-            auto wait_k = [&](int64_t cc) {
-                mbar_wait(&bars[C::B_KFULL + (int)(cc % S_)], (uint32_t)((cc / S_) & 1));
-                tc_fence_after();
             };
             for (int it = 0;; ++it) {
                 const int slot = it & 1;
@@ -423,13 +417,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                 for (int j = 0; j < I.n_chunks; ++j, ++c) {
                     const int s = (int)(c % S_);
                     const bool more = j + 1 < I.n_chunks;
-                    const int mn = more ? chunk_info<GATHER>(I, j + 1).mask : 0;
-                    bool have_k = false;
-                    if (mn & ~m) {  // tiles that start at c+1 only: give the tensor core work now
+                    int mn = 0;
+                    if (more) {
+                        mn = chunk_info<GATHER>(I, j + 1).mask;
                         wait_k(c + 1);
-                        have_k = true;
-                        if ((mn & ~m) & 1) issue_s(0, c + 1);
-                        if ((mn & ~m) & 2) issue_s(1, c + 1);
+                        if (mn & 1) issue_s(0, c + 1);
+                        if (mn & 2) issue_s(1, c + 1);
+                        mma_commit(&bars[C::B_KEMPTY + (int)((c + 1) % S_)]);
+                        if (j + 2 == I.n_chunks) mma_commit(&bars[C::B_QEMPTY]);
                     }
                     mbar_wait(&bars[C::B_VFULL + s], (uint32_t)((c / S_) & 1));
 #pragma unroll
@@ -437,19 +432,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                         if (!(m & (1 << t))) continue;
                         issue_pv(t, c, !started[t]);
                         started[t] = true;
-                        if (mn & m & (1 << t)) {
-                            if (!have_k) {
-                                wait_k(c + 1);
-                                have_k = true;
-                            }
-                            issue_s(t, c + 1);
-                        }
                     }
                     mma_commit(&bars[C::B_VEMPTY + s]);
-                    if (more) {
-                        mma_commit(&bars[C::B_KEMPTY + (int)((c + 1) % S_)]);
-                        if (j + 2 == I.n_chunks) mma_commit(&bars[C::B_QEMPTY]);
-                    }
                     m = mn;
                 }
             }
@@ -461,13 +445,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         const uint32_t quad = warp & 3u;
         const int r = (int)(quad * 32 + lane);
         const uint32_t lane_off = (quad * 32u) << 16;
-        const uint32_t tS = tmem_base + lane_off + (uint32_t)(256 * tile);
-        const uint32_t tO = tS + 128;
+        const uint32_t tO = tmem_base + lane_off + 128u * tile;
         const int row_in_item = 128 * tile + r;
-        const int blk = row_in_item / p.pq;  // membership bit 28 + blk
         const float sl2 = p.scale_log2;
         int64_t c = 0;
-        uint32_t ct = 0;  // this tile's chunk counter (SFULL/ODONE phases)
+        uint32_t ct = 0;  // this tile's chunk counter (S buffer = ct & 1)
         for (int it = 0;; ++it) {
             const int slot = it & 1;
             mbar_wait(&bars[C::B_IFULL + slot], (it >> 1) & 1);
@@ -483,39 +465,39 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             for (int j = 0; j < I.n_chunks; ++j, ++c) {
                 const int s = (int)(c % S_);
                 if (!(chunk_info<GATHER>(I, j).mask & (1 << tile))) continue;
-                uint32_t mw[4];
+                const int bi = (int)(ct & 1u);
+                const uint32_t tS = tmem_base + lane_off + s_col(tile, bi);
+                uint32_t mw[2];
                 if constexpr (GATHER) {
-                    mbar_wait(&bars[C::B_MFULL + s], (uint32_t)((c / S_) & 1));
-                    const uint32_t* meta = sMeta + s * C::kMetaWords;
-#pragma unroll
-                    for (int wd = 0; wd < 4; ++wd) mw[wd] = 0xffffffffu;  // membership is applied by the MMA
+                    mw[0] = mw[1] = 0xffffffffu;  // membership is applied by the MMA
                     if (p.causal) {
-                        int lo = 0, hi = 128;  // keys ascending: visible = prefix with key <= qrow
+                        mbar_wait(&bars[C::B_MFULL + s], (uint32_t)((c / S_) & 1));
+                        const uint32_t* meta = sMeta + s * kChunk;
+                        int lo = 0, hi = kChunk;  // keys ascending: visible = prefix with key <= qrow
                         while (lo < hi) {
                             const int mid = (lo + hi) >> 1;
                             if ((int64_t)meta[mid] <= qrow) lo = mid + 1;
                             else hi = mid;
                         }
-#pragma unroll
-                        for (int wd = 0; wd < 4; ++wd) mw[wd] &= prefix_mask(lo - 32 * wd);
+                        mw[0] = prefix_mask(lo);
+                        mw[1] = prefix_mask(lo - 32);
                     }
                 } else {
                     const int64_t vend = p.causal ? min(p.N, qrow + 1) : p.N;
-                    const int64_t nv = vend - (int64_t)j * 128;
-#pragma unroll
-                    for (int wd = 0; wd < 4; ++wd) mw[wd] = prefix_mask(nv - 32 * wd);
+                    const int64_t nv = vend - (int64_t)j * kChunk;
+                    mw[0] = prefix_mask(nv);
+                    mw[1] = prefix_mask(nv - 32);
                 }
-                const bool full = (mw[0] & mw[1] & mw[2] & mw[3]) == 0xffffffffu;
-                mbar_wait(&bars[C::B_SFULL + tile], ct & 1u);
+                const bool full = (mw[0] & mw[1]) == 0xffffffffu;
+                mbar_wait(&bars[C::B_SFULL + 2 * tile + bi], (ct >> 1) & 1u);
                 tc_fence_after();
                 __syncwarp();  // reconverge after the per-row causal search (tcgen05.ld is .sync.aligned)
-                // ---- pass 1: masked row max, 64 TMEM columns at a time
+                // ---- pass 1: masked row max over the chunk's 64 columns
                 float mx = -INFINITY;
-#pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
+                {
                     uint32_t a[32], b[32];
-                    tmem_ld32(tS + hf * 64, a);
-                    tmem_ld32(tS + hf * 64 + 32, b);
+                    tmem_ld32(tS, a);
+                    tmem_ld32(tS + 32, b);
                     tmem_ld_wait();
                     if (full) {
 #pragma unroll
@@ -524,11 +506,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                             mx = fmaxf(fmaxf(mx, __uint_as_float(b[t])), __uint_as_float(b[t + 1]));
                         }
                     } else {
-                        const uint32_t ma = mw[2 * hf], mb = mw[2 * hf + 1];
 #pragma unroll
                         for (int t = 0; t < 32; ++t) {
-                            const float va_ = (ma & (1u << t)) ? __uint_as_float(a[t]) : -INFINITY;
-                            const float vb_ = (mb & (1u << t)) ? __uint_as_float(b[t]) : -INFINITY;
+                            const float va_ = (mw[0] & (1u << t)) ? __uint_as_float(a[t]) : -INFINITY;
+                            const float vb_ = (mw[1] & (1u << t)) ? __uint_as_float(b[t]) : -INFINITY;
                             mx = fmaxf(fmaxf(mx, va_), vb_);
                         }
                     }
@@ -557,20 +538,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     }
                     tmem_st_wait();
                 }
-                // ---- pass 2: P = exp2(s*scale*log2e - m) (f32x2 FMA/ADD), bf16-packed over S_t.
-                // Half hf reads S columns [64hf, 64hf+64) and writes P columns [32hf, 32hf+32),
-                // which only cover S columns this thread already consumed.
-                const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
-                const uint64_t sl2x2 = pack_f32x2(sl2, sl2);
-                const uint64_t nmx2 = pack_f32x2(neg_m, neg_m);
-#pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
+                // ---- pass 2: P = exp2(s*scale*log2e - m) (f32x2 FMA/ADD), bf16-packed over S (32 cols)
+                {
+                    const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
+                    const uint64_t sl2x2 = pack_f32x2(sl2, sl2);
+                    const uint64_t nmx2 = pack_f32x2(neg_m, neg_m);
                     uint32_t a[32], b[32], pk[32];
-                    tmem_ld32(tS + hf * 64, a);
-                    tmem_ld32(tS + hf * 64 + 32, b);
+                    tmem_ld32(tS, a);
+                    tmem_ld32(tS + 32, b);
                     tmem_ld_wait();
-                    const uint32_t ma = full ? 0xffffffffu : mw[2 * hf];
-                    const uint32_t mb = full ? 0xffffffffu : mw[2 * hf + 1];
+                    const uint32_t ma = full ? 0xffffffffu : mw[0];
+                    const uint32_t mb = full ? 0xffffffffu : mw[1];
 #pragma unroll
                     for (int t = 0; t < 32; t += 2) {
                         const float2 xa = unpack_f32x2(
@@ -588,11 +566,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                         pk[t >> 1] = pack_bf16x2(p0, p1);
                         pk[16 + (t >> 1)] = pack_bf16x2(p2, p3);
                     }
-                    tmem_st32(tS + hf * 32, pk);
+                    tmem_st32(tS, pk);
+                    tmem_st_wait();
                 }
-                tmem_st_wait();
                 tc_fence_before();
-                mbar_arrive(&bars[C::B_PFULL + tile]);
+                mbar_arrive(&bars[C::B_PFULL + 2 * tile + bi]);
                 ++ct;
                 ++jt;
             }
@@ -744,14 +722,36 @@ __global__ void __launch_bounds__(kWlThreads) worklist_kernel(const int64_t* __r
             const int words = (int)min((int64_t)stripe_words, (N - ss + 31) / 32);
             for (int x = tid; x < 4 * stripe_words; x += kWlThreads) bm[x] = 0u;
             __syncthreads();
+            // Lists are sorted, so keys sharing a bitmap word sit in adjacent lanes: OR them
+            // within the warp (segmented by word) and issue one atomicOr per distinct word.
             for (int b = 0; b < nb; ++b) {
                 const int64_t a = offsets[r0 + b], e = offsets[r0 + b + 1];
-                for (int64_t t = a + tid; t < e; t += kWlThreads) {
-                    const int64_t key = indices[t];
-                    if (key >= ss && key < ss + stripe) {
-                        const int kk = (int)(key - ss);
-                        atomicOr(&bm[b * stripe_words + (kk >> 5)], 1u << (kk & 31));
+                constexpr int U = 8;  // independent loads in flight per thread
+                for (int64_t tb = a; tb < e; tb += (int64_t)kWlThreads * U) {
+                  int32_t kv[U];
+#pragma unroll
+                  for (int u = 0; u < U; ++u) {
+                      const int64_t t = tb + (int64_t)u * kWlThreads + tid;
+                      kv[u] = t < e ? __ldg(indices + t) : -1;
+                  }
+#pragma unroll
+                  for (int u = 0; u < U; ++u) {
+                    const int64_t key = kv[u];
+                    const bool in = key >= ss && key < ss + stripe;
+                    const int kk = in ? (int)(key - ss) : 0;
+                    const int word = in ? (kk >> 5) : -1 - (tid & 31);  // unique dummy per lane
+                    uint32_t bits = in ? (1u << (kk & 31)) : 0u;
+                    const int lane = tid & 31;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {  // suffix-OR over lanes with the same word
+                        const uint32_t ob = __shfl_down_sync(0xffffffffu, bits, o);
+                        const int ow = __shfl_down_sync(0xffffffffu, word, o);
+                        if (lane + o < 32 && ow == word) bits |= ob;
                     }
+                    const int pw = __shfl_up_sync(0xffffffffu, word, 1);
+                    const bool head = lane == 0 || pw != word;
+                    if (in && head) atomicOr(&bm[b * stripe_words + word], bits);
+                  }
                 }
             }
             __syncthreads();

@@ -113,4 +113,138 @@ cudaError_t launch_emit(const uint32_t* bitmask, int64_t words_per_row, const in
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------- fused plan
+// One CTA per 256-row attention item (G = 256/P_q selection rows).  From the
+// selection bitmask it emits the attention worklist of the item (attn.cu): the sorted
+// union of its rows' selections with one membership bit per row (entry = key |
+// bits << 28), split into three segments -- keys used by both 128-row tiles, by tile 0
+// only, by tile 1 only -- at the item's CSR base; segment lengths -> wl_len[3*item +
+// {0,1,2}] (if nnz <= wl_cap).  (CSR indices come from emit_kernel.)
+// Rounds of 256 bitmask words (lane = word, coalesced loads); per round a block-wide
+// exclusive scan of the 3 segment counts, entries staged in shared memory, then
+// written out coalesced.
+constexpr int kPlanThreads = 256;
+
+__global__ void __launch_bounds__(kPlanThreads) plan_kernel(const uint32_t* __restrict__ bitmask,
+                                                            int64_t words_per_row,
+                                                            const int64_t* __restrict__ offsets,
+                                                            const int64_t* __restrict__ d_nnz, int64_t wl_cap,
+                                                            uint32_t* __restrict__ wl, int32_t* __restrict__ wl_len,
+                                                            int64_t Np, int64_t n_it, int64_t N, int32_t pq,
+                                                            int32_t causal) {
+    __shared__ int sh[3][kPlanThreads / 32];
+    __shared__ uint32_t stage[kPlanThreads * 32];  // worst case: every bit of a round in one segment
+    const int64_t item = blockIdx.x;
+    const int64_t bh = item / n_it, it = item % n_it;
+    const int G = 256 / pq;
+    const int64_t i0 = it * G;
+    const int nb = (int)min((int64_t)G, Np - i0);
+    const int64_t r0 = bh * Np + i0;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (*d_nnz > wl_cap) {
+        if (tid == 0) wl_len[3 * item] = wl_len[3 * item + 1] = wl_len[3 * item + 2] = 0;
+        return;
+    }
+    int64_t vwords[4];
+    int64_t wmax = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const int64_t i = i0 + b;
+        const int64_t vis = b < nb ? (causal ? min(N, (i + 1) * (int64_t)pq) : N) : 0;
+        vwords[b] = (vis + 31) / 32;
+        wmax = max(wmax, vwords[b]);
+    }
+    const bool quad = G == 4;
+    // pass 1: segment totals (needed to place segments 1 and 2)
+    int c3[3] = {0, 0, 0};
+    for (int64_t x = tid; x < wmax; x += kPlanThreads) {
+        uint32_t bw[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+            bw[b] = (b < nb && x < vwords[b]) ? __ldg(bitmask + (r0 + b) * words_per_row + x) : 0u;
+        const uint32_t u0 = quad ? (bw[0] | bw[1]) : bw[0];
+        const uint32_t u1 = quad ? (bw[2] | bw[3]) : bw[1];
+        c3[0] += __popc(u0 & u1);
+        c3[1] += __popc(u0 & ~u1);
+        c3[2] += __popc(u1 & ~u0);
+    }
+    int tot[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        int v = c3[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) sh[k][w] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        int t = 0;
+        for (int x = 0; x < kPlanThreads / 32; ++x) t += sh[k][x];
+        tot[k] = t;
+    }
+    __syncthreads();
+    const int64_t base = offsets[r0];
+    int64_t run[3] = {base, base + tot[0], base + tot[0] + tot[1]};
+    // pass 2: rounds of kPlanThreads words
+    for (int64_t x0 = 0; x0 < wmax; x0 += kPlanThreads) {
+        const int64_t x = x0 + tid;
+        uint32_t bw[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+            bw[b] = (b < nb && x < vwords[b]) ? __ldg(bitmask + (r0 + b) * words_per_row + x) : 0u;
+        const uint32_t u0 = quad ? (bw[0] | bw[1]) : bw[0];
+        const uint32_t u1 = quad ? (bw[2] | bw[3]) : bw[1];
+        const uint32_t seg[3] = {u0 & u1, u0 & ~u1, u1 & ~u0};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int cnt = __popc(seg[k]);
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int n = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += n;
+            }
+            if (lane == 31) sh[k][w] = incl;
+            __syncthreads();
+            int before = 0, round_tot = 0;
+            for (int y = 0; y < kPlanThreads / 32; ++y) {
+                const int t = sh[k][y];
+                before += (y < w) ? t : 0;
+                round_tot += t;
+            }
+            int pos = before + incl - cnt;
+            uint32_t m = seg[k];
+            while (m) {
+                const int bit = __ffs(m) - 1;
+                const uint32_t mb = 1u << bit;
+                const uint32_t mem = ((bw[0] & mb) ? 1u : 0u) | ((bw[1] & mb) ? 2u : 0u) | ((bw[2] & mb) ? 4u : 0u) |
+                                     ((bw[3] & mb) ? 8u : 0u);
+                stage[pos++] = (uint32_t)(x * 32 + bit) | (mem << 28);
+                m &= m - 1;
+            }
+            __syncthreads();
+            for (int t = tid; t < round_tot; t += kPlanThreads) wl[run[k] + t] = stage[t];
+            run[k] += round_tot;
+            __syncthreads();
+        }
+    }
+    if (tid == 0) {
+        wl_len[3 * item] = tot[0];
+        wl_len[3 * item + 1] = tot[1];
+        wl_len[3 * item + 2] = tot[2];
+    }
+}
+
+cudaError_t launch_plan(const uint32_t* bitmask, int64_t words_per_row, const int64_t* offsets, const int64_t* d_nnz,
+                        int64_t wl_cap, uint32_t* wl, int32_t* wl_len, int64_t BH, int64_t Np, int64_t N, int32_t pq,
+                        int32_t causal, cudaStream_t st) {
+    const int64_t n_it = (N + 255) / 256;
+    const int64_t items = BH * n_it;
+    if (items <= 0) return cudaSuccess;
+    plan_kernel<<<(unsigned)items, kPlanThreads, 0, st>>>(bitmask, words_per_row, offsets, d_nnz, wl_cap, wl, wl_len,
+                                                          Np, n_it, N, pq, causal);
+    return cudaGetLastError();
+}
+
 }  // namespace va

@@ -195,6 +195,35 @@ vecattn_status_t cuda_status(cudaError_t e) {
     return VECATTN_ERR_CUDA;
 }
 
+
+// Pooling + the selection GEMM passes of the configured mode + scan (counts -> offsets).
+cudaError_t run_select(const vecattn_problem_t* p, const vecattn_select_params_t* s, const void* q, const void* k,
+                       int64_t* offsets, int64_t* d_nnz, const SelectWs& w, SelectParams& sp, cudaStream_t cs) {
+    const int64_t R = sp.BH * sp.Np;
+    auto run = [&](int epi, int pass) -> cudaError_t {
+        plan_segments(p, s, epi, sp);
+        sp.pass = pass;
+        if (set_k_map(p, k, epi == va::EPI_TOPK_HIST ? 128 : 256, sp) != VECATTN_OK) return cudaErrorInvalidValue;
+        return va::launch_select(sp, epi, (int)p->D, cs);
+    };
+    cudaError_t e = va::launch_pool(q, w.qp, sp.BH, p->N, p->D, s->pq, cs);
+    if (e == cudaSuccess) e = cudaMemsetAsync(w.counts, 0, (size_t)R * 8, cs);
+    if (e == cudaSuccess) {
+        if (s->mode == VECATTN_SEL_MINS_ALG1) {
+            e = run(va::EPI_ALG1, 0);
+        } else if (s->mode == VECATTN_SEL_MINS_EXACT) {
+            e = cudaMemsetAsync(w.rowmax, 0, (size_t)R * 4, cs);
+            if (e == cudaSuccess) e = run(va::EPI_MAX, 0);
+            if (e == cudaSuccess) e = run(va::EPI_THRESH, 0);
+        } else {
+            for (int pass = 0; pass < 4 && e == cudaSuccess; ++pass) e = run(va::EPI_TOPK_HIST, pass);
+            if (e == cudaSuccess) e = run(va::EPI_TOPK_EMIT, 0);
+        }
+    }
+    if (e == cudaSuccess) e = va::launch_scan(w.counts, R, offsets, d_nnz, cs);
+    return e;
+}
+
 #define VA_CU(x)                                            \
     do {                                                    \
         cudaError_t e_ = (x);                               \
@@ -269,28 +298,7 @@ vecattn_status_t vecattn_select(const vecattn_problem_t* p, const vecattn_select
     SelectParams* sp = new SelectParams;
     st = fill_select_params(p, s, s->pq, k, w, *sp);
     if (st != VECATTN_OK) { delete sp; return st; }
-    const int64_t R = sp->BH * sp->Np;
-    auto run = [&](int epi, int pass) -> cudaError_t {
-        plan_segments(p, s, epi, *sp);
-        sp->pass = pass;
-        if (set_k_map(p, k, epi == va::EPI_TOPK_HIST ? 128 : 256, *sp) != VECATTN_OK) return cudaErrorInvalidValue;
-        return va::launch_select(*sp, epi, (int)p->D, cs);
-    };
-    cudaError_t e = va::launch_pool(q, w.qp, sp->BH, p->N, p->D, s->pq, cs);
-    if (e == cudaSuccess) e = cudaMemsetAsync(w.counts, 0, (size_t)R * 8, cs);
-    if (e == cudaSuccess) {
-        if (s->mode == VECATTN_SEL_MINS_ALG1) {
-            e = run(va::EPI_ALG1, 0);
-        } else if (s->mode == VECATTN_SEL_MINS_EXACT) {
-            e = cudaMemsetAsync(w.rowmax, 0, (size_t)R * 4, cs);
-            if (e == cudaSuccess) e = run(va::EPI_MAX, 0);
-            if (e == cudaSuccess) e = run(va::EPI_THRESH, 0);
-        } else {
-            for (int pass = 0; pass < 4 && e == cudaSuccess; ++pass) e = run(va::EPI_TOPK_HIST, pass);
-            if (e == cudaSuccess) e = run(va::EPI_TOPK_EMIT, 0);
-        }
-    }
-    if (e == cudaSuccess) e = va::launch_scan(w.counts, R, offsets, d_nnz, cs);
+    cudaError_t e = run_select(p, s, q, k, offsets, d_nnz, w, *sp, cs);
     if (e == cudaSuccess && indices && cap > 0)
         e = va::launch_emit(w.bitmask, sp->words_per_row, offsets, d_nnz, cap, indices, sp->BH, sp->Np, p->N,
                             s->pq, p->causal ? 1 : 0, cs);
@@ -410,8 +418,8 @@ vecattn_status_t vecattn_dense_fwd(const vecattn_problem_t* p, const void* q, co
     AttnParams* ap = new AttnParams;
     st = attn_common(p, q, k, v, o, lse, *ap);
     if (st == VECATTN_OK &&
-        (!tmap_3d(&ap->tm_k, k, (uint64_t)p->D, (uint64_t)p->N, (uint64_t)(p->B * p->Hkv), 128) ||
-         !tmap_3d(&ap->tm_v, v, (uint64_t)p->D, (uint64_t)p->N, (uint64_t)(p->B * p->Hkv), 128)))
+        (!tmap_3d(&ap->tm_k, k, (uint64_t)p->D, (uint64_t)p->N, (uint64_t)(p->B * p->Hkv), 64) ||
+         !tmap_3d(&ap->tm_v, v, (uint64_t)p->D, (uint64_t)p->N, (uint64_t)(p->B * p->Hkv), 64)))
         st = VECATTN_ERR_UNSUPPORTED;
     if (st != VECATTN_OK) { delete ap; return st; }
     ap->Np = (p->N + 127) / 128;
@@ -435,6 +443,62 @@ vecattn_status_t vecattn_validate_selection(const vecattn_problem_t* p, int32_t 
                                                                   p->causal ? 1 : 0, d_bad);
     VA_CU(cudaGetLastError());
     return VECATTN_OK;
+}
+
+
+size_t vecattn_forward_workspace_bytes(const vecattn_problem_t* p, const vecattn_select_params_t* s,
+                                       int64_t nnz_cap) {
+    if (check_problem(p) != VECATTN_OK || !s || (s->pq != 64 && s->pq != 128) || nnz_cap < 0) return 0;
+    return carve_select(p, s->pq, nullptr).total + vecattn_sparse_workspace_bytes(p, s->pq, nnz_cap);
+}
+
+vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_select_params_t* s, const void* q,
+                                 const void* k, const void* v, int64_t* offsets, int32_t* indices, int64_t cap,
+                                 int64_t* d_nnz, int64_t nnz_cap, void* o, float* lse, void* ws, size_t ws_bytes,
+                                 vecattn_stream_t stream) {
+    vecattn_status_t st = check_select(p, s);
+    if (st != VECATTN_OK) return st;
+    if (!q || !k || !v || !o || !offsets || !d_nnz || cap < 0 || (cap > 0 && !indices) || nnz_cap < 0)
+        return VECATTN_ERR_INVALID_ARGUMENT;
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return VECATTN_ERR_SHAPE;
+    const size_t need = vecattn_forward_workspace_bytes(p, s, nnz_cap);
+    if (!ws || ws_bytes < need) return VECATTN_ERR_WORKSPACE;
+    if (!aligned16(ws)) return VECATTN_ERR_SHAPE;
+    cudaStream_t cs = (cudaStream_t)stream;
+    const SelectWs w = carve_select(p, s->pq, ws);
+    uint8_t* b = static_cast<uint8_t*>(ws) + w.total;
+    SelectParams* sp = new SelectParams;
+    AttnParams* ap = new AttnParams;
+    st = fill_select_params(p, s, s->pq, k, w, *sp);
+    if (st == VECATTN_OK) st = attn_common(p, q, k, v, o, lse, *ap);
+    const int64_t rows_kv = p->B * p->Hkv * p->N;
+    if (st == VECATTN_OK && (!tmap_gather(&ap->tm_k, k, (uint64_t)p->D, (uint64_t)rows_kv) ||
+                             !tmap_gather(&ap->tm_v, v, (uint64_t)p->D, (uint64_t)rows_kv)))
+        st = VECATTN_ERR_UNSUPPORTED;
+    if (st != VECATTN_OK) { delete sp; delete ap; return st; }
+    uint32_t* wl = reinterpret_cast<uint32_t*>(b);
+    int32_t* wl_len = reinterpret_cast<int32_t*>(b + align_up((size_t)nnz_cap * 4));
+    int* counter = reinterpret_cast<int*>(b + align_up((size_t)nnz_cap * 4) + align_up((size_t)(ap->BH * ap->n_mt) * 12));
+    ap->Np = sp->Np;
+    ap->pq = s->pq;
+    ap->wl = wl;
+    ap->offsets = offsets;
+    ap->wl_len = wl_len;
+    ap->work_counter = counter;
+    ap->d_nnz = d_nnz;
+    ap->nnz_cap = nnz_cap;
+    cudaError_t e = run_select(p, s, q, k, offsets, d_nnz, w, *sp, cs);
+    if (e == cudaSuccess && indices && cap > 0)
+        e = va::launch_emit(w.bitmask, sp->words_per_row, offsets, d_nnz, cap, indices, sp->BH, sp->Np, p->N, s->pq,
+                            p->causal ? 1 : 0, cs);
+    if (e == cudaSuccess)
+        e = va::launch_plan(w.bitmask, sp->words_per_row, offsets, d_nnz, nnz_cap, wl, wl_len, sp->BH, sp->Np, p->N,
+                            s->pq, p->causal ? 1 : 0, cs);
+    if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, sizeof(int), cs);
+    if (e == cudaSuccess) e = va::launch_attn(*ap, (int)p->D, true, attn_grid(ap->total_items), cs);
+    delete sp;
+    delete ap;
+    return cuda_status(e);
 }
 
 }  // extern "C"

@@ -58,6 +58,12 @@ cudaError_t launch_emit(const uint32_t* bitmask, int64_t words_per_row, const in
                         const int64_t* d_nnz, int64_t cap, int32_t* indices, int64_t BH, int64_t Np,
                         int64_t N, int32_t pq, int32_t causal, cudaStream_t st);
 
+// Fused select->attend plan: the 3-segment attention worklist per 256-row item,
+// straight from the selection bitmask (see compact.cu).
+cudaError_t launch_plan(const uint32_t* bitmask, int64_t words_per_row, const int64_t* offsets, const int64_t* d_nnz,
+                        int64_t wl_cap, uint32_t* wl, int32_t* wl_len, int64_t BH, int64_t Np, int64_t N, int32_t pq,
+                        int32_t causal, cudaStream_t st);
+
 // ----------------------------------------------------------------------- attention
 struct AttnParams {
     alignas(64) CUtensorMap tm_q;  // 3-D {D, N, B*Hq}, box {64, 128, 1}
@@ -72,6 +78,8 @@ struct AttnParams {
     const int64_t* offsets;        // gather: CSR offsets [B*Hq*Np + 1] (item base = offsets[bh*Np + (256/pq)*item])
     const int32_t* wl_len;         // gather: [B*Hq*n_mt][3] union segment lengths (both tiles | tile 0 | tile 1)
     int* work_counter;             // dynamic tile scheduler (zeroed before launch)
+    const int64_t* d_nnz;          // fused path: skip all work if *d_nnz > nnz_cap (capacity protocol)
+    int64_t nnz_cap;
     int64_t N, Np, BH, Hq, Hkv, n_mt /* 256-row items per head */, total_items;
     int32_t pq, causal;
     float scale, scale_log2;

@@ -55,6 +55,13 @@ WORKLOADS = {
     "dit128k": Workload("dit128k", 1, 24, 24, 131072, 128, False, 8192, (32, 64, 64), 4),
     "vlm128k": Workload("vlm128k", 1, 28, 4, 131072, 128, True, 16, (32, 64, 64), 5),
 }
+# SURVEY.md 8(d) sweep: F x 64 x 64 VIDEO grids, N = 16K..256K, DiT-like and VLM-like
+for _f in (4, 8, 16, 32, 64):
+    _n = _f * 64 * 64
+    WORKLOADS[f"dit{_n // 1024}k"] = WORKLOADS.get(f"dit{_n // 1024}k") or Workload(
+        f"dit{_n // 1024}k", 1, 24, 24, _n, 128, False, 8192, (_f, 64, 64), 10 + _f)
+    WORKLOADS[f"vlm{_n // 1024}k"] = WORKLOADS.get(f"vlm{_n // 1024}k") or Workload(
+        f"vlm{_n // 1024}k", 1, 28, 4, _n, 128, True, 16, (_f, 64, 64), 100 + _f)
 
 
 def _gen(seed: int, device) -> torch.Generator:

@@ -63,6 +63,8 @@ def load(path: str = LIB_PATH):
         "vecattn_sparse_fwd": (i32, [prob, i32, vp, vp, vp, vp, vp, i64, vp, vp, vp, sz, vp]),
         "vecattn_dense_workspace_bytes": (sz, [prob]),
         "vecattn_dense_fwd": (i32, [prob, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "vecattn_forward_workspace_bytes": (sz, [prob, sel, i64]),
+        "vecattn_forward": (i32, [prob, sel, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp, vp, sz, vp]),
         "vecattn_validate_selection": (i32, [prob, i32, vp, vp, vp, vp]),
         "vecattn_debug_scores": (i32, [prob, i32, vp, vp, vp, vp, sz, vp]),
         "vecattn_status_string": (ctypes.c_char_p, [i32]),
@@ -79,6 +81,7 @@ def load(path: str = LIB_PATH):
 
 EXPORTED = ["vecattn_pool", "vecattn_select_workspace_bytes", "vecattn_select", "vecattn_sparse_workspace_bytes",
             "vecattn_sparse_fwd", "vecattn_dense_workspace_bytes", "vecattn_dense_fwd",
+            "vecattn_forward_workspace_bytes", "vecattn_forward",
             "vecattn_validate_selection", "vecattn_debug_scores", "vecattn_status_string", "vecattn_last_cuda_error",
             "vecattn_abi_version"]
 
@@ -260,6 +263,47 @@ def dense_fwd(q, k, v, causal: bool = False, scale=None, with_lse: bool = True, 
     ws = torch.empty(256, dtype=torch.uint8, device=q.device)
     dense_fwd_into(q, k, v, o, lse, ws, causal, scale, stream)
     return o, lse
+
+
+def forward_workspace_bytes(pr: Problem, cfg: SelectConfig, nnz_cap: int) -> int:
+    return int(load().vecattn_forward_workspace_bytes(ctypes.byref(pr), ctypes.byref(cfg.params()), int(nnz_cap)))
+
+
+def forward_into(q, k, v, cfg: SelectConfig, offsets, indices, cap: int, d_nnz, nnz_cap: int, o, lse,
+                 ws: torch.Tensor, causal: bool, scale=None, stream=None):
+    """Raw vecattn_forward (fused selection + sparse attention) into caller buffers."""
+    lib = load()
+    _dev_check(q, k, v, offsets, indices, d_nnz, o, lse)
+    pr = problem(q, k, causal, scale)
+    sp = cfg.params()
+    rc = lib.vecattn_forward(ctypes.byref(pr), ctypes.byref(sp), _ptr(q), _ptr(k), _ptr(v), _ptr(offsets),
+                             _ptr(indices), int(cap), _ptr(d_nnz), int(nnz_cap), _ptr(o), _ptr(lse), _ptr(ws),
+                             ws.numel(), _stream(stream))
+    _check("vecattn_forward", rc)
+
+
+def forward(q, k, v, cfg: SelectConfig, causal: bool = False, scale=None, nnz_cap: int | None = None,
+            want_indices: bool = True, stream=None):
+    """Fused VecAttention forward: returns (o, lse, offsets, indices-or-None)."""
+    B, H, N, D = q.shape
+    Np = (N + cfg.pq - 1) // cfg.pq
+    pr = problem(q, k, causal, scale)
+    offsets = torch.empty(B * H * Np + 1, dtype=torch.int64, device=q.device)
+    d_nnz = torch.empty(1, dtype=torch.int64, device=q.device)
+    o = torch.empty_like(q)
+    lse = torch.empty(B, H, N, dtype=torch.float32, device=q.device)
+    if nnz_cap is None:  # counts-only selection to size the plan (one host sync)
+        wsel = torch.empty(select_workspace_bytes(pr, cfg), dtype=torch.uint8, device=q.device)
+        select_into(q, k, cfg, offsets, None, 0, d_nnz, wsel, causal, scale, stream)
+        nnz_cap = max(1, int(d_nnz.item()))
+    ws = torch.empty(forward_workspace_bytes(pr, cfg, nnz_cap), dtype=torch.uint8, device=q.device)
+    indices = torch.empty(nnz_cap, dtype=torch.int32, device=q.device) if want_indices else None
+    forward_into(q, k, v, cfg, offsets, indices, nnz_cap if want_indices else 0, d_nnz, nnz_cap, o, lse, ws,
+                 causal, scale, stream)
+    nnz = int(d_nnz.item())
+    if nnz > nnz_cap:
+        return forward(q, k, v, cfg, causal, scale, nnz, want_indices, stream)
+    return o, lse, offsets, (indices[:nnz] if want_indices else None)
 
 
 def validate_selection(offsets, indices, q_shape, pq: int, causal: bool, stream=None) -> int:

@@ -218,3 +218,56 @@ def test_sparse_degenerate_rows_and_empty_blocks():
         ro, rl = orc.sparse_attn(bf16_np(q[0, 0]), bf16_np(k[0, 0]), bf16_np(v[0, 0]), off.cpu().numpy(),
                                  idx.cpu().numpy(), pq, causal=causal)
         check_attn(bf16_np(o[0, 0]), lse[0, 0].cpu().numpy(), ro, rl, f"degenerate causal={causal}")
+
+
+# ------------------------------------------------------------------ fused forward
+FWD_CASES = [
+    ("video", 1, 4, 2, 8192 + 100, 128, 64, True, dict(mode="alg1", alpha=1.0, gk=16)),
+    ("gauss", 1, 2, 1, 4096 + 96, 128, 64, False, dict(mode="alg1", alpha=0.4, gk=16)),
+    ("video", 1, 2, 2, 5000, 128, 128, True, dict(mode="exact", alpha=1.2)),
+    ("gauss", 1, 1, 1, 1024, 64, 64, False, dict(mode="topk", keep_frac=0.25)),
+    ("video", 1, 2, 1, 6000, 64, 64, False, dict(mode="alg1", alpha=1.5, gk=8192)),
+]
+
+
+@pytest.mark.parametrize("case", FWD_CASES, ids=[f"{c[0]}-N{c[4]}-D{c[5]}-pq{c[6]}-{'c' if c[7] else 'nc'}"
+                                                 for c in FWD_CASES])
+def test_fused_forward_equals_two_call_path_and_oracle(case):
+    kind, B, Hq, Hkv, N, D, pq, causal, sel = case
+    q, k, v, qd, kd, vd = make(kind, B, Hq, Hkv, N, D)
+    cfg = va.SelectConfig(pq=pq, **sel)
+    o, lse, off, idx = va.forward(qd, kd, vd, cfg, causal=causal)
+    off2, idx2 = va.select(qd, kd, cfg, causal=causal)
+    o2, lse2 = va.sparse_fwd(qd, kd, vd, off2, idx2, pq=pq, causal=causal)
+    torch.cuda.synchronize()
+    assert torch.equal(off, off2) and torch.equal(idx, idx2)      # same selection, same CSR
+    assert torch.equal(o, o2) and torch.equal(lse, lse2)          # same plan order -> bit-identical
+    off_h, idx_h = off.cpu().numpy(), idx.cpu().numpy()
+    Np = (N + pq - 1) // pq
+    blocks = np.array(sorted(set([0, Np // 2, Np - 1])), np.int64)
+    for h in range(Hq):
+        kv = h // (Hq // Hkv)
+        r0 = h * Np
+        ro, rl = orc.sparse_attn(bf16_np(q[0, h]), bf16_np(k[0, kv]), bf16_np(v[0, kv]),
+                                 off_h[r0:r0 + Np + 1] - off_h[r0], idx_h[off_h[r0]:off_h[r0 + Np]], pq,
+                                 causal=causal, blocks=blocks)
+        rows = (blocks[:, None] * pq + np.arange(pq)[None, :]).reshape(-1)
+        ok = rows < N
+        check_attn(bf16_np(o[0, h])[rows[ok]], lse[0, h].cpu().numpy()[rows[ok]], ro[ok], rl[ok], f"fwd h{h}")
+
+
+def test_fused_forward_capacity_protocol():
+    q, k, v, qd, kd, vd = make("gauss", 1, 1, 1, 2048, 128)
+    cfg = va.SelectConfig(mode="alg1", pq=64, alpha=0.4)
+    pr = va.problem(qd, kd, False)
+    off = torch.empty(33, dtype=torch.int64, device=dev())
+    nnz = torch.empty(1, dtype=torch.int64, device=dev())
+    o = torch.full_like(qd, 7.0)
+    lse = torch.empty(1, 1, 2048, device=dev())
+    small = 16
+    ws = torch.empty(va.forward_workspace_bytes(pr, cfg, small), dtype=torch.uint8, device=dev())
+    va.forward_into(qd, kd, vd, cfg, off, None, 0, nnz, small, o, lse, ws, False)
+    n = int(nnz.item())
+    assert n > small and bool((o == 7.0).all())   # plan capacity too small: attention skipped
+    o2, lse2, off2, idx2 = va.forward(qd, kd, vd, cfg, nnz_cap=small)  # binding retries with nnz
+    assert idx2.numel() == n
