@@ -440,6 +440,10 @@ def run_ours(args):
     peaks = load_peaks()
     achieved = sp_flops / (sparse_ms_avg * 1e-3) / 1e12  # this rank's sparse_fwd call (incl. worklist)
     peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp) and args.workload == "dit128k" and ws == 1:
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
     line = {
         "metric": "select+sparse attention at 128K tokens (DiT H=24, rho=0.785): effective dense-equivalent "
                   "TFLOP/s (ms_per_step, speedup vs in-library dense in extra keys)",
@@ -470,7 +474,8 @@ def run_ours(args):
         "sparse_achieved_tflops": round(achieved, 2),
         "roofline": {"bound": "tensor", "kernel": "attn_kernel<128,gather> (timed as the vecattn_sparse_fwd call)",
                      "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
-                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_note": "dram read+write bytes per launch from profiles/traffic.json (ncu --set full)",
                      "peak_source": peaks["source"] + " bf16 sustained",
                      "algorithmic": "4*D*sum_r |J_r| flops per launch (DESIGN.md 'Rooflines')"},
         "clocks": clocks,

@@ -74,6 +74,15 @@ struct AttnCfg {
 
 VA_DEV uint32_t s_col(int t, int b) { return 256u + 128u * t + 64u * b; }
 
+// Debug timeline (p.trace != null): CTA 0 records clock64() per chunk and event kind
+// (0 K issue, 1 V issue, 2 K landed, 3 V landed, 4/5 PV0/PV1 issued, 6/7 S0 ready/P0 done,
+// 8/9 S1 ready/P1 done) -- scripts/trace_run.py.
+constexpr int kTraceChunks = 4096;
+VA_DEV void trace(const AttnParams& p, int kind, int64_t c) {
+    if (p.trace != nullptr && blockIdx.x == 0 && c < kTraceChunks)
+        p.trace[(int64_t)kind * kTraceChunks + c] = clock64();
+}
+
 struct Item {
     int64_t bh, it;  // head, 256-row item within the head
     int n_chunks;
@@ -296,6 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     const uint32_t key = e & kKeyMask;
                     const int row = (int)(bh_kv * p.N + (ok ? key : 0u));
                     if (lane == 0 && round > 0) mbar_wait(&bars[bempty + s], (round - 1) & 1);
+                    if (lane == 0 && sub == 0) trace(p, isK ? 0 : 1, c);
                     __syncwarp();
                     if (isK) {
                         // K_ext row: bias 0 for member blocks, -2^100 (bf16 0xF180) otherwise
@@ -355,6 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             auto wait_k = [&](int64_t cc) {
                 mbar_wait(&bars[C::B_KFULL + (int)(cc % S_)], (uint32_t)((cc / S_) & 1));
                 tc_fence_after();
+                trace(p, 2, cc);
             };
             auto issue_s = [&](int t, int64_t cc) {
                 const int s = (int)(cc % S_);
@@ -427,11 +438,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                         if (j + 2 == I.n_chunks) mma_commit(&bars[C::B_QEMPTY]);
                     }
                     mbar_wait(&bars[C::B_VFULL + s], (uint32_t)((c / S_) & 1));
+                    trace(p, 3, c);
 #pragma unroll
                     for (int t = 0; t < 2; ++t) {
                         if (!(m & (1 << t))) continue;
                         issue_pv(t, c, !started[t]);
                         started[t] = true;
+                        trace(p, 4 + t, c);
                     }
                     mma_commit(&bars[C::B_VEMPTY + s]);
                     m = mn;
@@ -491,6 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                 const bool full = (mw[0] & mw[1]) == 0xffffffffu;
                 mbar_wait(&bars[C::B_SFULL + 2 * tile + bi], (ct >> 1) & 1u);
                 tc_fence_after();
+                if (lane == 0 && (warp == 2 || warp == 6)) trace(p, 6 + 2 * tile, c);
                 __syncwarp();  // reconverge after the per-row causal search (tcgen05.ld is .sync.aligned)
                 // ---- pass 1: masked row max over the chunk's 64 columns
                 float mx = -INFINITY;
@@ -571,6 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                 }
                 tc_fence_before();
                 mbar_arrive(&bars[C::B_PFULL + 2 * tile + bi]);
+                if (lane == 0 && (warp == 2 || warp == 6)) trace(p, 7 + 2 * tile, c);
                 ++ct;
                 ++jt;
             }

@@ -212,6 +212,25 @@ VA_DEV float2 fadd2(float2 a, float2 b) {
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pack_f32x2(a.x, a.y)), "l"(pack_f32x2(b.x, b.y)));
     return unpack_f32x2(d);
 }
+// exp2 on the FMA pipe for two lanes (FA4-style MUFU offload): round-to-nearest split
+// x = i + f (f in [-0.5, 0.5]) via the 1.5*2^23 magic add, 2^f by a degree-3 minimax
+// polynomial (max relative error 1.0e-4, well below bf16's 2^-9), 2^i by an integer add
+// to the exponent field.  Inputs clamped at -125 (results below 2^-125 are ~0 anyway).
+VA_DEV float2 ex2_poly2(float x0, float x1) {
+    x0 = fmaxf(x0, -125.f);
+    x1 = fmaxf(x1, -125.f);
+    const uint64_t X = pack_f32x2(x0, x1);
+    const uint64_t T = ffma2(X, pack_f32x2(1.f, 1.f), pack_f32x2(12582912.f, 12582912.f));
+    const uint64_t R = ffma2(T, pack_f32x2(1.f, 1.f), pack_f32x2(-12582912.f, -12582912.f));
+    const uint64_t F = ffma2(R, pack_f32x2(-1.f, -1.f), X);
+    uint64_t P = ffma2(F, pack_f32x2(0.054993368685245514f, 0.054993368685245514f),
+                       pack_f32x2(0.24221104383468628f, 0.24221104383468628f));
+    P = ffma2(P, F, pack_f32x2(0.693286120891571f, 0.693286120891571f));
+    P = ffma2(P, F, pack_f32x2(1.f, 1.f));
+    const float2 p = unpack_f32x2(P), t = unpack_f32x2(T);
+    return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                       __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
 // Order-preserving map fp32 -> u32 (a < b  <=>  key(a) < key(b) for non-NaN).
 VA_DEV uint32_t f32_order_key(float f) {
     uint32_t u = __float_as_uint(f);

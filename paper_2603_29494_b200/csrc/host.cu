@@ -356,6 +356,10 @@ static vecattn_status_t attn_common(const vecattn_problem_t* p, const void* q, c
     ap.causal = p->causal ? 1 : 0;
     ap.scale = scale;
     ap.scale_log2 = scale * 1.4426950408889634f;
+    {   // debug timeline: VECATTN_TRACE=<device pointer as decimal> (tests/scripts only)
+        const char* tr = getenv("VECATTN_TRACE");
+        ap.trace = tr ? reinterpret_cast<long long*>(strtoull(tr, nullptr, 10)) : nullptr;
+    }
     if (!tmap_3d(&ap.tm_q, q, (uint64_t)p->D, (uint64_t)p->N, (uint64_t)ap.BH, 128)) return VECATTN_ERR_UNSUPPORTED;
     return VECATTN_OK;
 }

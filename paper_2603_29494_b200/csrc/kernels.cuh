@@ -80,6 +80,7 @@ struct AttnParams {
     int* work_counter;             // dynamic tile scheduler (zeroed before launch)
     const int64_t* d_nnz;          // fused path: skip all work if *d_nnz > nnz_cap (capacity protocol)
     int64_t nnz_cap;
+    long long* trace;              // debug timeline [10][4096] clock64 (CTA 0) or null
     int64_t N, Np, BH, Hq, Hkv, n_mt /* 256-row items per head */, total_items;
     int32_t pq, causal;
     float scale, scale_log2;

@@ -61,5 +61,16 @@ if os.path.exists(rep):
         summary[name] = d
         lines += [f"### `{name}`", ""] + [f"- {k}: {v}" for k, v in d.items()] + [""]
 open(os.path.join(out_dir, f"ncu_{tag}.md"), "w").write("\n".join(lines) + "\n")
+# per-launch DRAM traffic of the sparse attention kernel (bench.py roofline.traffic)
+for name, d in summary.items():
+    if "attn_kernel<128, 1>" in name or "attn_kernel<128, true>" in name:
+        def num(x):
+            v, u = x.split()[0], x.split()[1] if len(x.split()) > 1 else ""
+            mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(u, 1)
+            return float(v) * mult
+        tr = num(d["dram__bytes_read.sum"]) + num(d["dram__bytes_write.sum"])
+        json.dump({"kernel": name, "dram_bytes_per_launch": tr, "source": f"profiles/ncu_{tag}.md",
+                   "workload": "dit128k, 24 heads, vecattn_forward"},
+                  open(os.path.join(out_dir, "traffic.json"), "w"), indent=1)
 json.dump(summary, open(os.path.join(out_dir, f"ncu_{tag}.json"), "w"), indent=1)
 print("\n".join(lines))
