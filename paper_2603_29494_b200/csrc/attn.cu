@@ -63,7 +63,7 @@ struct AttnCfg {
                          B_VFULL = B_KEMPTY + kStages, B_VEMPTY = B_VFULL + kStages,
                          B_MFULL = B_VEMPTY + kStages, B_SFULL = B_MFULL + kStages /* [2 tiles][2 bufs] */,
                          B_PFULL = B_SFULL + 4, B_ODONE = B_PFULL + 4, B_OEMPTY = B_ODONE + 2,
-                         B_IFULL = B_OEMPTY + 2, B_IEMPTY = B_IFULL + 2, kNumBars = B_IEMPTY + 2;
+                         B_IFULL = B_OEMPTY + 2, B_IEMPTY = B_IFULL + 2, B_OFIN = B_IEMPTY + 2, kNumBars = B_OFIN + 2;
     static constexpr int kOffItem = kOffBar + kNumBars * 8;
     static constexpr int kSmem = kOffItem + 16;
     // TMEM: O_t at 128t (D cols); S[t][b] at 256 + 128t + 64b (64 cols; P over its first 32)
@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             mbar_init(&bars[C::B_OEMPTY + t], 128);
             mbar_init(&bars[C::B_IFULL + t], 1);
             mbar_init(&bars[C::B_IEMPTY + t], 1 + kSoftmaxThreads + kLoadWarps);
+            mbar_init(&bars[C::B_OFIN + t], 1);
         }
         fence_barrier_init();
     }
@@ -449,6 +450,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     mma_commit(&bars[C::B_VEMPTY + s]);
                     m = mn;
                 }
+                // O_0 / O_1 final for this item (one phase per item with chunks, both tiles)
+                mma_commit(&bars[C::B_OFIN + 0]);
+                mma_commit(&bars[C::B_OFIN + 1]);
             }
         }
         __syncwarp();
@@ -463,6 +467,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         const float sl2 = p.scale_log2;
         int64_t c = 0;
         uint32_t ct = 0;  // this tile's chunk counter (S buffer = ct & 1)
+        uint32_t od = 0;  // ODONE phases known complete (= PVs of this tile known finished)
+        uint32_t fi = 0;  // OFIN phases waited (items with chunks)
         for (int it = 0;; ++it) {
             const int slot = it & 1;
             mbar_wait(&bars[C::B_IFULL + slot], (it >> 1) & 1);
@@ -506,33 +512,36 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                 tc_fence_after();
                 if (lane == 0 && (warp == 2 || warp == 6)) trace(p, 6 + 2 * tile, c);
                 __syncwarp();  // reconverge after the per-row causal search (tcgen05.ld is .sync.aligned)
-                // ---- pass 1: masked row max over the chunk's 64 columns
-                float mx = -INFINITY;
-                {
-                    uint32_t a[32], b[32];
-                    tmem_ld32(tS, a);
-                    tmem_ld32(tS + 32, b);
-                    tmem_ld_wait();
-                    if (full) {
+                // ---- single TMEM pass (TMEM reads, 64 B/clk/SM, bind at D = 128): S -> registers,
+                // masked row max, lazy O rescale, P = exp2(s*scale*log2e - m) bf16-packed over S.
+                uint32_t a[32], b[32];
+                tmem_ld32(tS, a);
+                tmem_ld32(tS + 32, b);
+                tmem_ld_wait();
+                if (!full) {  // causal / ragged tail only: masked scores -> -inf (exp2 -> 0)
 #pragma unroll
-                        for (int t = 0; t < 32; t += 2) {
-                            mx = fmaxf(fmaxf(mx, __uint_as_float(a[t])), __uint_as_float(a[t + 1]));
-                            mx = fmaxf(fmaxf(mx, __uint_as_float(b[t])), __uint_as_float(b[t + 1]));
-                        }
-                    } else {
-#pragma unroll
-                        for (int t = 0; t < 32; ++t) {
-                            const float va_ = (mw[0] & (1u << t)) ? __uint_as_float(a[t]) : -INFINITY;
-                            const float vb_ = (mw[1] & (1u << t)) ? __uint_as_float(b[t]) : -INFINITY;
-                            mx = fmaxf(fmaxf(mx, va_), vb_);
-                        }
+                    for (int t = 0; t < 32; ++t) {
+                        a[t] = (mw[0] & (1u << t)) ? a[t] : 0xff800000u;
+                        b[t] = (mw[1] & (1u << t)) ? b[t] : 0xff800000u;
                     }
                 }
-                const float m_new = fmaxf(m_ref, mx * sl2);
-                if (jt > 0) {  // O_t stable (PV_t of this tile's previous chunk done) before a rescale
-                    mbar_wait(&bars[C::B_ODONE + tile], (ct - 1) & 1u);
-                    tc_fence_after();
+                float mx;
+                {  // 4 independent FMNMX3 chains (latency), then combine
+                    float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+                    for (int t = 0; t < 32; t += 4) {
+                        m4[0] = fmaxf(fmaxf(m4[0], __uint_as_float(a[t])), __uint_as_float(a[t + 1]));
+                        m4[1] = fmaxf(fmaxf(m4[1], __uint_as_float(a[t + 2])), __uint_as_float(a[t + 3]));
+                        m4[2] = fmaxf(fmaxf(m4[2], __uint_as_float(b[t])), __uint_as_float(b[t + 1]));
+                        m4[3] = fmaxf(fmaxf(m4[3], __uint_as_float(b[t + 2])), __uint_as_float(b[t + 3]));
+                    }
+                    mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
                 }
+                const float m_new = fmaxf(m_ref, mx * sl2);
+                // SFULL(ct) fired, so every MMA issued before S(ct) -- including PV(ct-2) of
+                // this tile -- is complete: ODONE phases 0..ct-2 are done (parity waits on
+                // phase ct-1 are then unambiguous).
+                if (ct >= 1 && od < ct - 1) od = ct - 1;
                 const bool need = m_new > m_ref + 8.0f;
                 const float corr = need ? ex2(m_ref - m_new) : 1.0f;
                 if (need) {
@@ -541,41 +550,33 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     m_ref = m_new;
                 }
                 if (jt > 0 && __any_sync(0xffffffffu, need)) {
+                    // O_t must be stable (PV_t of this tile's previous chunk done) before the
+                    // rescale; without a rescale the softmax never waits on the PV pipeline.
+                    for (; od < ct; ++od) mbar_wait(&bars[C::B_ODONE + tile], od & 1u);
+                    tc_fence_after();
 #pragma unroll
-                    for (int g = 0; g < D / 32; ++g) {
-                        uint32_t o[32];
-                        tmem_ld32(tO + g * 32, o);
+                    for (int g = 0; g < D / 8; ++g) {
+                        uint32_t o[8];
+                        tmem_ld8(tO + g * 8, o);
                         tmem_ld_wait();
 #pragma unroll
-                        for (int t = 0; t < 32; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * corr);
-                        tmem_st32(tO + g * 32, o);
+                        for (int t = 0; t < 8; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * corr);
+                        tmem_st8(tO + g * 8, o);
                     }
                     tmem_st_wait();
                 }
-                // ---- pass 2: P = exp2(s*scale*log2e - m) (f32x2 FMA/ADD), bf16-packed over S (32 cols)
                 {
                     const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
                     const uint64_t sl2x2 = pack_f32x2(sl2, sl2);
                     const uint64_t nmx2 = pack_f32x2(neg_m, neg_m);
-                    uint32_t a[32], b[32], pk[32];
-                    tmem_ld32(tS, a);
-                    tmem_ld32(tS + 32, b);
-                    tmem_ld_wait();
-                    const uint32_t ma = full ? 0xffffffffu : mw[0];
-                    const uint32_t mb = full ? 0xffffffffu : mw[1];
+                    uint32_t pk[32];
 #pragma unroll
                     for (int t = 0; t < 32; t += 2) {
                         const float2 xa = unpack_f32x2(
                             ffma2(pack_f32x2(__uint_as_float(a[t]), __uint_as_float(a[t + 1])), sl2x2, nmx2));
                         const float2 xb = unpack_f32x2(
                             ffma2(pack_f32x2(__uint_as_float(b[t]), __uint_as_float(b[t + 1])), sl2x2, nmx2));
-                        float p0 = ex2(xa.x), p1 = ex2(xa.y), p2 = ex2(xb.x), p3 = ex2(xb.y);
-                        if (!full) {
-                            p0 = (ma & (1u << t)) ? p0 : 0.f;
-                            p1 = (ma & (2u << t)) ? p1 : 0.f;
-                            p2 = (mb & (1u << t)) ? p2 : 0.f;
-                            p3 = (mb & (2u << t)) ? p3 : 0.f;
-                        }
+                        const float p0 = ex2(xa.x), p1 = ex2(xa.y), p2 = ex2(xb.x), p3 = ex2(xb.y);
                         lsum2 = fadd2(lsum2, fadd2(make_float2(p0, p1), make_float2(p2, p3)));
                         pk[t >> 1] = pack_bf16x2(p0, p1);
                         pk[16 + (t >> 1)] = pack_bf16x2(p2, p3);
@@ -594,9 +595,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             const float l = (m_ref < -1e28f) ? 0.f : lsum2.x + lsum2.y;
             const float inv = l > 0.f ? 1.f / l : 0.f;
             __nv_bfloat16* orow = p.o + (I.bh * p.N + qrow) * D;
+            if (I.n_chunks > 0) {  // every PV of the item complete (ODONE parity may be 2 behind here)
+                mbar_wait(&bars[C::B_OFIN + tile], fi & 1u);
+                ++fi;
+            }
             if (jt > 0) {
                 __syncwarp();
-                mbar_wait(&bars[C::B_ODONE + tile], (ct - 1) & 1u);
                 tc_fence_after();
 #pragma unroll
                 for (int g = 0; g < D / 32; ++g) {
