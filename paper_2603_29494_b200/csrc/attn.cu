@@ -190,11 +190,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         mbar_init(&bars[C::B_QFULL], 1);
         mbar_init(&bars[C::B_QEMPTY], 1);
         for (int s = 0; s < S_; ++s) {
-            mbar_init(&bars[C::B_KFULL + s], GATHER ? 2 : 1);
+            mbar_init(&bars[C::B_KFULL + s], 1);
             mbar_init(&bars[C::B_KEMPTY + s], 1);
-            mbar_init(&bars[C::B_VFULL + s], GATHER ? 2 : 1);
+            mbar_init(&bars[C::B_VFULL + s], 1);
             mbar_init(&bars[C::B_VEMPTY + s], 1);
-            mbar_init(&bars[C::B_MFULL + s], 2);
+            mbar_init(&bars[C::B_MFULL + s], 1);
         }
         for (int x = 0; x < 4; ++x) {
             mbar_init(&bars[C::B_SFULL + x], 1);
@@ -265,19 +265,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         }
     } else if (warp >= kFirstLoadWarp) {
         // ======================================== K/V loaders (4 warps)
-        // Warps 10-11 load K, 12-13 load V; warp (g & 1) owns chunk columns [32*(g&1), +32).
-        // GATHER: one plan entry per lane (prefetched one chunk ahead); lanes 0-7 issue one
-        // tile::gather4 per 128-B column block.  K loaders also write the K_ext bias rows
-        // (consumed by the S MMA, freed with KEMPTY); V loaders publish the keys for the
-        // causal mask (freed with VEMPTY).  K and V rings are decoupled.
+        // Warp g owns every chunk c = g (mod 4): K and V of all 64 keys.  A warp's TMA issue
+        // rate is bound by a fixed per-iteration cost plus ~70 clk per gather4 (uniform-register
+        // setup), so whole chunks per warp (fewer iterations each) beat splitting every chunk
+        // across warps (scripts/ubench_gather.cu).  Stage s = c % S_ with S_ % 4 == 0, so the
+        // previous chunk on a stage is this warp's own and its EMPTY parity waits are exact.
+        // GATHER: two plan entries per lane (keys lane, 32+lane; prefetched one owned chunk
+        // ahead), lanes 0-15 issue the tile::gather4s; K_ext bias rows are written before the
+        // K gathers (consumed by the S MMA, freed with KEMPTY), the keys for the causal mask
+        // before the V gathers (freed with VEMPTY).
+        static_assert(S_ % kLoadWarps == 0, "stage ownership");
         const int g = (int)warp - kFirstLoadWarp;
-        const bool isK = g < 2;
-        const int sub = g & 1;
-        uint8_t* ring = isK ? sK : sV;
-        const void* tmap = isK ? (const void*)&p.tm_k : (const void*)&p.tm_v;
-        const int bfull = isK ? C::B_KFULL : C::B_VFULL;
-        const int bempty = isK ? C::B_KEMPTY : C::B_VEMPTY;
-        int64_t c = 0;
+        int64_t c = 0;  // chunks of all previous items
         for (int it = 0;; ++it) {
             const int slot = it & 1;
             mbar_wait(&bars[C::B_IFULL + slot], (it >> 1) & 1);
@@ -289,69 +288,107 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             if (I.n_chunks == 0) continue;
             const int64_t b = I.bh / p.Hq, h = I.bh % p.Hq;
             const int64_t bh_kv = b * p.Hkv + h / (p.Hq / p.Hkv);
+            int j = (int)(((int64_t)g - c % kLoadWarps + kLoadWarps) % kLoadWarps);  // first owned chunk
             if constexpr (GATHER) {
                 const uint32_t* wlp = p.wl + I.base;
-                const int col = 32 * sub + (int)lane;
-                Chunk ch = chunk_info<true>(I, 0);
-                uint32_t e = col < ch.len ? __ldg(wlp + ch.start + col) : 0u;
-                for (int j = 0; j < I.n_chunks; ++j, ++c) {
-                    const int s = (int)(c % S_);
-                    const int round = (int)(c / S_);
-                    const bool ok = col < ch.len;
+                Chunk ch;
+                ch.len = 0;
+                ch.start = 0;
+                if (j < I.n_chunks) ch = chunk_info<true>(I, j);
+                uint32_t e0 = (int)lane < ch.len ? __ldg(wlp + ch.start + lane) : 0u;
+                uint32_t e1 = 32 + (int)lane < ch.len ? __ldg(wlp + ch.start + 32 + lane) : 0u;
+                for (; j < I.n_chunks; j += kLoadWarps) {
+                    const int64_t cc = c + j;
+                    const int s = (int)(cc % S_);
+                    const int round = (int)(cc / S_);
                     Chunk chn;
                     chn.len = 0;
                     chn.start = 0;
-                    if (j + 1 < I.n_chunks) chn = chunk_info<true>(I, j + 1);
-                    const uint32_t en = col < chn.len ? __ldg(wlp + chn.start + col) : 0u;
-                    const uint32_t key = e & kKeyMask;
-                    const int row = (int)(bh_kv * p.N + (ok ? key : 0u));
-                    if (lane == 0 && round > 0) mbar_wait(&bars[bempty + s], (round - 1) & 1);
-                    if (lane == 0 && sub == 0) trace(p, isK ? 0 : 1, c);
-                    __syncwarp();
-                    if (isK) {
-                        // K_ext row: bias 0 for member blocks, -2^100 (bf16 0xF180) otherwise
-                        const uint32_t mem = ok ? (e >> 28) : 0u;
-                        const uint32_t b0 = (mem & 1u) ? 0u : 0xF180u, b1 = (mem & 2u) ? 0u : 0xF180u;
-                        const uint32_t b2 = (mem & 4u) ? 0u : 0xF180u, b3 = (mem & 8u) ? 0u : 0xF180u;
-                        *reinterpret_cast<uint4*>(smem + C::kOffKx + s * kChunk * 16 * 2 + k16_offset(col, 0)) =
-                            make_uint4(b0 | (b1 << 16), b2 | (b3 << 16), 0u, 0u);
-                        fence_proxy_async();  // generic-proxy smem write -> tcgen05.mma (async proxy)
-                    } else {
-                        sMeta[s * kChunk + col] = ok ? key : kPad;
-                    }
-                    __syncwarp();
-                    if (lane == 0) {
-                        if (!isK) mbar_arrive(&bars[C::B_MFULL + s]);
-                        mbar_arrive_expect_tx(&bars[bfull + s], 32 * D * 2);
-                    }
+                    if (j + kLoadWarps < I.n_chunks) chn = chunk_info<true>(I, j + kLoadWarps);
+                    const uint32_t en0 = (int)lane < chn.len ? __ldg(wlp + chn.start + lane) : 0u;
+                    const uint32_t en1 = 32 + (int)lane < chn.len ? __ldg(wlp + chn.start + 32 + lane) : 0u;
+                    const bool ok0 = (int)lane < ch.len, ok1 = 32 + (int)lane < ch.len;
+                    const uint32_t key0 = e0 & kKeyMask, key1 = e1 & kKeyMask;
+                    const int r0 = (int)(bh_kv * p.N + (ok0 ? key0 : 0u));
+                    const int r1 = (int)(bh_kv * p.N + (ok1 ? key1 : 0u));
                     const int q0 = (4 * (int)lane) & 31;
-                    const int ra = __shfl_sync(0xffffffffu, row, q0), rb = __shfl_sync(0xffffffffu, row, q0 + 1);
-                    const int rc = __shfl_sync(0xffffffffu, row, q0 + 2), rd = __shfl_sync(0xffffffffu, row, q0 + 3);
+                    const int a0 = __shfl_sync(0xffffffffu, r0, q0), a1 = __shfl_sync(0xffffffffu, r0, q0 + 1);
+                    const int a2 = __shfl_sync(0xffffffffu, r0, q0 + 2), a3 = __shfl_sync(0xffffffffu, r0, q0 + 3);
+                    const int b0_ = __shfl_sync(0xffffffffu, r1, q0), b1_ = __shfl_sync(0xffffffffu, r1, q0 + 1);
+                    const int b2_ = __shfl_sync(0xffffffffu, r1, q0 + 2), b3_ = __shfl_sync(0xffffffffu, r1, q0 + 3);
+                    const bool lo = lane < 8;
+                    const int ra = lo ? a0 : b0_, rb = lo ? a1 : b1_, rc = lo ? a2 : b2_, rd = lo ? a3 : b3_;
+                    // ---- K: bias rows, then the gathers
+                    if (lane == 0 && round > 0) mbar_wait(&bars[C::B_KEMPTY + s], (round - 1) & 1);
+                    if (lane == 0) trace(p, 0, cc);
                     __syncwarp();
-                    if (lane < 8) {
-                        uint8_t* dst = ring + s * C::kKVBytes + (32 * sub + 4 * (int)lane) * 128;
+                    {
+                        // K_ext row: bias 0 for member blocks, -2^100 (bf16 0xF180) otherwise
+                        uint8_t* kx = smem + C::kOffKx + s * kChunk * 16 * 2;
+                        const uint32_t m0 = ok0 ? (e0 >> 28) : 0u, m1 = ok1 ? (e1 >> 28) : 0u;
+                        auto bias = [](uint32_t mem) {
+                            const uint32_t x0 = (mem & 1u) ? 0u : 0xF180u, x1 = (mem & 2u) ? 0u : 0xF180u;
+                            const uint32_t x2 = (mem & 4u) ? 0u : 0xF180u, x3 = (mem & 8u) ? 0u : 0xF180u;
+                            return make_uint4(x0 | (x1 << 16), x2 | (x3 << 16), 0u, 0u);
+                        };
+                        *reinterpret_cast<uint4*>(kx + k16_offset((int)lane, 0)) = bias(m0);
+                        *reinterpret_cast<uint4*>(kx + k16_offset(32 + (int)lane, 0)) = bias(m1);
+                        fence_proxy_async();  // generic-proxy smem write -> tcgen05.mma (async proxy)
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_expect_tx(&bars[C::B_KFULL + s], kChunk * D * 2);
+                    if (lane < 16) {
+                        uint8_t* dst = sK + s * C::kKVBytes + 4 * (int)lane * 128;
 #pragma unroll
                         for (int cb = 0; cb < C::kCB; ++cb)
-                            tma_gather4(dst + cb * kChunk * 128, tmap, &bars[bfull + s], cb * 64, ra, rb, rc, rd);
+                            tma_gather4(dst + cb * kChunk * 128, &p.tm_k, &bars[C::B_KFULL + s], cb * 64, ra, rb, rc,
+                                        rd);
                     }
-                    e = en;
+                    // ---- V: keys for the causal mask, then the gathers
+                    if (lane == 0 && round > 0) mbar_wait(&bars[C::B_VEMPTY + s], (round - 1) & 1);
+                    if (lane == 0) trace(p, 1, cc);
+                    __syncwarp();
+                    sMeta[s * kChunk + lane] = ok0 ? key0 : kPad;
+                    sMeta[s * kChunk + 32 + lane] = ok1 ? key1 : kPad;
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(&bars[C::B_MFULL + s]);
+                        mbar_arrive_expect_tx(&bars[C::B_VFULL + s], kChunk * D * 2);
+                    }
+                    if (lane < 16) {
+                        uint8_t* dst = sV + s * C::kKVBytes + 4 * (int)lane * 128;
+#pragma unroll
+                        for (int cb = 0; cb < C::kCB; ++cb)
+                            tma_gather4(dst + cb * kChunk * 128, &p.tm_v, &bars[C::B_VFULL + s], cb * 64, ra, rb, rc,
+                                        rd);
+                    }
+                    e0 = en0;
+                    e1 = en1;
                     ch = chn;
                 }
             } else {
-                for (int j = 0; j < I.n_chunks; ++j, ++c) {
-                    if (sub != 0 || lane != 0) continue;
-                    const int s = (int)(c % S_);
-                    const int round = (int)(c / S_);
-                    if (round > 0) mbar_wait(&bars[bempty + s], (round - 1) & 1);
-                    uint8_t* dst = ring + s * C::kKVBytes;
-                    mbar_arrive_expect_tx(&bars[bfull + s], C::kKVBytes);
+                if (lane == 0) {
+                    for (; j < I.n_chunks; j += kLoadWarps) {
+                        const int64_t cc = c + j;
+                        const int s = (int)(cc % S_);
+                        const int round = (int)(cc / S_);
+                        if (round > 0) mbar_wait(&bars[C::B_KEMPTY + s], (round - 1) & 1);
+                        mbar_arrive_expect_tx(&bars[C::B_KFULL + s], C::kKVBytes);
 #pragma unroll
-                    for (int cb = 0; cb < C::kCB; ++cb)
-                        tma_load_3d(dst + cb * kChunk * 128, tmap, &bars[bfull + s], cb * 64, j * kChunk,
-                                    (int)bh_kv);
+                        for (int cb = 0; cb < C::kCB; ++cb)
+                            tma_load_3d(sK + s * C::kKVBytes + cb * kChunk * 128, &p.tm_k, &bars[C::B_KFULL + s],
+                                        cb * 64, j * kChunk, (int)bh_kv);
+                        if (round > 0) mbar_wait(&bars[C::B_VEMPTY + s], (round - 1) & 1);
+                        mbar_arrive_expect_tx(&bars[C::B_VFULL + s], C::kKVBytes);
+#pragma unroll
+                        for (int cb = 0; cb < C::kCB; ++cb)
+                            tma_load_3d(sV + s * C::kKVBytes + cb * kChunk * 128, &p.tm_v, &bars[C::B_VFULL + s],
+                                        cb * 64, j * kChunk, (int)bh_kv);
+                    }
                 }
                 __syncwarp();
             }
+            c += I.n_chunks;
         }
     } else if (warp == 1) {
         // ======================================== MMA issuer (single thread)
