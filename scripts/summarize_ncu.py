@@ -29,11 +29,12 @@ if os.path.exists(lf):
     def mean(sub):
         xs = [x for k, v in ours.items() if sub in k for x in v]
         return sum(xs) / len(xs) if xs else 0.0
-    step = {n: mean(n) for n in ["pool_kernel", "select_kernel", "scan_kernel", "emit_kernel", "worklist_kernel"]}
+    # one vecattn_forward step (the bench's timed call): pool, select, scan, emit (CSR), plan, attention
+    step = {n: mean(n) for n in ["pool_kernel", "select_kernel", "scan_kernel", "emit_kernel", "plan_kernel"]}
     sp = [x for k, v in ours.items() if "attn_kernel<128, 1>" in k or "attn_kernel<128, true>" in k for x in v]
     step["attn_kernel<gather>"] = sum(sp) / len(sp) if sp else 0.0
     tot = sum(step.values())
-    lines += ["", "Per-step shares (one select + sparse pass):", "", "| stage | ms | share |", "|---|---|---|"]
+    lines += ["", "Per-step shares (one vecattn_forward call = the bench step):", "", "| stage | ms | share |", "|---|---|---|"]
     for n, t in step.items():
         lines.append(f"| {n} | {t:.3f} | {100*t/tot:.1f}% |")
     lines.append(f"| total | {tot:.3f} | 100% |")
@@ -50,8 +51,11 @@ if os.path.exists(rep):
             "lts__t_sector_hit_rate.pct", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
             "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
             "smsp__inst_executed.sum", "sm__cycles_elapsed.avg.per_second", "launch__grid_size",
+            "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+            "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active",
             "launch__block_size"]
-    lines += ["", "## --set full (one launch each; `--heads 4` variant of the bench workload)", ""]
+    lines += ["", "## --set full (one launch; full bench workload, 24 heads, vecattn_forward)", ""]
     for r in rows[2:]:
         name = r[h.index("Kernel Name")]
         d = {}
