@@ -332,6 +332,8 @@ def run_ours(args):
 
     clk = ClockSampler(local)
     timers = []
+    stage = []  # library-recorded (select, emit+plan, attention) ms per timed step
+    va.kernel_timing(True)
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -340,7 +342,9 @@ def run_ours(args):
     for _ in range(args.steps):
         flush.zero_()  # L2 flush between timed steps (outside the events)
         step(timers)
+        stage.append(va.kernel_timing_last())
     torch.cuda.synchronize()
+    va.kernel_timing(False)
     if ws > 1:
         dist.barrier()
     clocks = clk.stop()
@@ -438,7 +442,23 @@ def run_ours(args):
     total_dense = dense_flops(B * H, N, D, causal)
     value = total_dense / (step_ms * 1e-3) / 1e12
     peaks = load_peaks()
-    achieved = sp_flops / (sparse_ms_avg * 1e-3) / 1e12  # this rank's sparse_fwd call (incl. worklist)
+    attn_ms = statistics.mean(x[2] for x in stage)  # the attention kernel alone, CUDA events on its stream
+    sel_stage_ms = statistics.mean(x[0] for x in stage)
+    plan_stage_ms = statistics.mean(x[1] for x in stage)
+    achieved = sp_flops / (attn_ms * 1e-3) / 1e12
+    tt2 = torch.tensor([attn_ms, sel_stage_ms, plan_stage_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(tt2, op=dist.ReduceOp.MAX)
+    attn_ms, sel_stage_ms, plan_stage_ms = (float(x) for x in tt2)
+    # selection stage (pool + pooled-score GEMM/filter + offsets scan): algorithmic HBM bytes,
+    # Q read (pool), Q_p write + read, K read once per KV head, bitmask write,
+    # counts + offsets
+    Npq = (N + pq - 1) // pq
+    sel_bytes = B * Hl * (2 * N * D + 4 * Npq * D + Npq * ((N + 255) // 256) * 32 + 16 * Npq) + \
+        B * max(1, Hkv * Hl // H) * 2 * N * D
+    sel_bytes_all = torch.tensor([float(sel_bytes)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(sel_bytes_all)
     peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -472,7 +492,15 @@ def run_ours(args):
         "speedup_vs_dense": round(dense_ms / step_ms, 3) if dense_ms else None,
         "dense_tflops": round(total_dense / (dense_ms * 1e-3) / 1e12, 2) if dense_ms else None,
         "sparse_achieved_tflops": round(achieved, 2),
-        "roofline": {"bound": "tensor", "kernel": "attn_kernel<128,gather> (timed as the vecattn_sparse_fwd call)",
+        "stage_ms": {"select": round(sel_stage_ms, 4), "emit_plan": round(plan_stage_ms, 4),
+                     "attention": round(attn_ms, 4),
+                     "note": "CUDA events recorded by the library on the launching stream (vecattn_kernel_timing)"},
+        "select_roofline": {"bound": "hbm", "achieved": round(float(sel_bytes_all[0]) / ws / (sel_stage_ms * 1e-3) / 1e9, 1),
+                            "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                            "frac": round(float(sel_bytes_all[0]) / ws / (sel_stage_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
+                            "algorithmic_bytes": int(sel_bytes_all[0] / ws),
+                            "note": "pool + selection GEMM/filter + scan; SURVEY 8(d): tensor/issue-bound at rho >= 0.75"},
+        "roofline": {"bound": "tensor", "kernel": "attn_kernel<128,gather> (attention kernel alone, vecattn_forward)",
                      "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "traffic_note": "dram read+write bytes per launch from profiles/traffic.json (ncu --set full)",

@@ -158,6 +158,16 @@ VECATTN_API vecattn_status_t vecattn_validate_selection(const vecattn_problem_t*
 VECATTN_API vecattn_status_t vecattn_debug_scores(const vecattn_problem_t* p, int32_t pq, const void* q, const void* k,
                                       float* scores, void* ws, size_t ws_bytes, vecattn_stream_t stream);
 
+/* Measurement hook (bench.py roofline).  When enabled, every vecattn_forward /
+ * vecattn_sparse_fwd / vecattn_dense_fwd call records CUDA events on its stream around
+ * (a) query pooling + the selection GEMM/filter + offsets scan, (b) CSR emission + the
+ * attention plan, and (c) the attention kernel alone.  Library-owned events, one set per
+ * process (not thread-safe; for benchmarking only).  vecattn_kernel_timing_last waits for
+ * the events of the most recent timed call and returns the three durations in ms (-1 for a
+ * stage the call did not run).  Disabled by default: no events are recorded.            */
+VECATTN_API vecattn_status_t vecattn_kernel_timing(int32_t enable);
+VECATTN_API vecattn_status_t vecattn_kernel_timing_last(float* select_ms, float* plan_ms, float* attn_ms);
+
 VECATTN_API const char* vecattn_status_string(vecattn_status_t s);
 /* Text of the last CUDA error that made an entry point return VECATTN_ERR_CUDA (this thread). */
 VECATTN_API const char* vecattn_last_cuda_error(void);

@@ -253,6 +253,46 @@ extern "C" {
 
 int32_t vecattn_abi_version(void) { return 1; }
 
+// ------------------------------------------------------------------ measurement hook
+namespace {
+struct Timing {
+    bool enabled = false;
+    bool created = false;
+    bool has_sel = false, has_plan = false, has_attn = false;
+    cudaEvent_t ev[4];  // select start, select end / plan start, plan end / attn start, attn end
+};
+Timing g_timing;
+void tmark(int i, cudaStream_t st) {
+    if (g_timing.enabled) cudaEventRecord(g_timing.ev[i], st);
+}
+void tbegin(bool sel, bool plan) {
+    g_timing.has_sel = sel;
+    g_timing.has_plan = plan;
+    g_timing.has_attn = true;
+}
+}  // namespace
+
+vecattn_status_t vecattn_kernel_timing(int32_t enable) {
+    if (enable && !g_timing.created) {
+        for (auto& e : g_timing.ev)
+            if (cudaEventCreate(&e) != cudaSuccess) return cuda_status(cudaGetLastError());
+        g_timing.created = true;
+    }
+    g_timing.enabled = enable != 0;
+    return VECATTN_OK;
+}
+
+vecattn_status_t vecattn_kernel_timing_last(float* select_ms, float* plan_ms, float* attn_ms) {
+    if (!select_ms || !plan_ms || !attn_ms) return VECATTN_ERR_INVALID_ARGUMENT;
+    *select_ms = *plan_ms = *attn_ms = -1.f;
+    if (!g_timing.created) return VECATTN_OK;
+    if (cudaEventSynchronize(g_timing.ev[3]) != cudaSuccess) return cuda_status(cudaGetLastError());
+    if (g_timing.has_sel) cudaEventElapsedTime(select_ms, g_timing.ev[0], g_timing.ev[1]);
+    if (g_timing.has_plan) cudaEventElapsedTime(plan_ms, g_timing.ev[1], g_timing.ev[2]);
+    if (g_timing.has_attn) cudaEventElapsedTime(attn_ms, g_timing.ev[2], g_timing.ev[3]);
+    return VECATTN_OK;
+}
+
 const char* vecattn_last_cuda_error(void) { return cudaGetErrorString(g_last_cuda_error); }
 
 const char* vecattn_status_string(vecattn_status_t s) {
@@ -398,10 +438,14 @@ vecattn_status_t vecattn_sparse_fwd(const vecattn_problem_t* p, int32_t pq, cons
     ap->offsets = offsets;
     ap->wl_len = wl_len;
     ap->work_counter = counter;
+    if (g_timing.enabled) tbegin(false, true);
+    tmark(1, cs);
     cudaError_t e = va::launch_worklist(offsets, indices ? indices : reinterpret_cast<const int32_t*>(wl), wl, wl_len,
                                         ap->BH, ap->Np, ap->n_mt, p->N, pq, cs);
     if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, sizeof(int), cs);
+    tmark(2, cs);
     if (e == cudaSuccess) e = va::launch_attn(*ap, (int)p->D, true, attn_grid(ap->total_items), cs);
+    tmark(3, cs);
     delete ap;
     return cuda_status(e);
 }
@@ -430,7 +474,10 @@ vecattn_status_t vecattn_dense_fwd(const vecattn_problem_t* p, const void* q, co
     ap->pq = 128;
     ap->work_counter = reinterpret_cast<int*>(ws);
     cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(int), cs);
+    if (g_timing.enabled) tbegin(false, false);
+    tmark(2, cs);
     if (e == cudaSuccess) e = va::launch_attn(*ap, (int)p->D, false, attn_grid(ap->total_items), cs);
+    tmark(3, cs);
     delete ap;
     return cuda_status(e);
 }
@@ -491,7 +538,10 @@ vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_selec
     ap->work_counter = counter;
     ap->d_nnz = d_nnz;
     ap->nnz_cap = nnz_cap;
+    if (g_timing.enabled) tbegin(true, true);
+    tmark(0, cs);
     cudaError_t e = run_select(p, s, q, k, offsets, d_nnz, w, *sp, cs);
+    tmark(1, cs);
     if (e == cudaSuccess && indices && cap > 0)
         e = va::launch_emit(w.bitmask, sp->words_per_row, offsets, d_nnz, cap, indices, sp->BH, sp->Np, p->N, s->pq,
                             p->causal ? 1 : 0, cs);
@@ -499,7 +549,9 @@ vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_selec
         e = va::launch_plan(w.bitmask, sp->words_per_row, offsets, d_nnz, nnz_cap, wl, wl_len, sp->BH, sp->Np, p->N,
                             s->pq, p->causal ? 1 : 0, cs);
     if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, sizeof(int), cs);
+    tmark(2, cs);
     if (e == cudaSuccess) e = va::launch_attn(*ap, (int)p->D, true, attn_grid(ap->total_items), cs);
+    tmark(3, cs);
     delete sp;
     delete ap;
     return cuda_status(e);

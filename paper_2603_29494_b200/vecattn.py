@@ -70,6 +70,8 @@ def load(path: str = LIB_PATH):
         "vecattn_status_string": (ctypes.c_char_p, [i32]),
         "vecattn_last_cuda_error": (ctypes.c_char_p, []),
         "vecattn_abi_version": (i32, []),
+        "vecattn_kernel_timing": (i32, [i32]),
+        "vecattn_kernel_timing_last": (i32, [P(ctypes.c_float), P(ctypes.c_float), P(ctypes.c_float)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -83,7 +85,20 @@ EXPORTED = ["vecattn_pool", "vecattn_select_workspace_bytes", "vecattn_select", 
             "vecattn_sparse_fwd", "vecattn_dense_workspace_bytes", "vecattn_dense_fwd",
             "vecattn_forward_workspace_bytes", "vecattn_forward",
             "vecattn_validate_selection", "vecattn_debug_scores", "vecattn_status_string", "vecattn_last_cuda_error",
-            "vecattn_abi_version"]
+            "vecattn_abi_version", "vecattn_kernel_timing", "vecattn_kernel_timing_last"]
+
+
+def kernel_timing(enable: bool) -> None:
+    """Enable/disable the library's per-stage CUDA-event timing (vecattn_kernel_timing)."""
+    _check("vecattn_kernel_timing", load().vecattn_kernel_timing(1 if enable else 0))
+
+
+def kernel_timing_last() -> tuple[float, float, float]:
+    """(select_ms, plan_ms, attn_ms) of the most recent timed call; -1 for stages it did not run."""
+    a, b_, c = ctypes.c_float(), ctypes.c_float(), ctypes.c_float()
+    _check("vecattn_kernel_timing_last", load().vecattn_kernel_timing_last(ctypes.byref(a), ctypes.byref(b_),
+                                                                             ctypes.byref(c)))
+    return a.value, b_.value, c.value
 
 
 def _ptr(t):
