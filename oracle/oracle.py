@@ -59,6 +59,8 @@ def _load():
         lib.oracle_scores_row.argtypes = [pd, pd, i64, i64, d, i64, pd]
         lib.oracle_select_rows.argtypes = [pd, pd, i64, i64, i32, i32, d, i32, i32, i32, d, i64, d,
                                            pi64, i64, pi64, pi32, i64, pd, pi64]
+        lib.oracle_topp_rows.argtypes = [pd, pd, i64, i64, i32, i32, d, d, pi64, i64, pi64, ctypes.POINTER(ctypes.c_int32),
+                                         i64, pd]
         lib.oracle_attn_blocks.argtypes = [pd, pd, pd, i64, i64, i32, i32, d, pi64, i64, pi64,
                                            pi32, pd, pd]
         lib.oracle_dense_rows.argtypes = [pd, pd, pd, i64, i64, i32, d, pi64, i64, pd, pd]
@@ -170,6 +172,32 @@ def select(qp, k, pq: int, *, causal: bool = False, mode: int = SEL_MINS_ALG1, b
     if detail:
         return offsets, indices, thr, js
     return offsets, indices
+
+
+def select_topp(qp, k, pq: int, p: float, *, causal: bool = False, scale: float | None = None, rows=None,
+                detail: bool = False):
+    """topP selection of the naive approach for one head: per pooled
+    row, the smallest set of keys in descending softmax(s) order whose mass is >= p.
+    Returns CSR (offsets, indices) over the requested pooled rows; detail=True also returns
+    the selected mass per row."""
+    qp, k = _f64(qp), _f64(k)
+    N, D = k.shape
+    Np = qp.shape[0]
+    scale = default_scale(D) if scale is None else float(scale)
+    rows = np.arange(Np, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, np.int64)
+    R = rows.size
+    counts = np.zeros(R, np.int64)
+    idx = np.empty((R, N), np.int32)
+    mass = np.empty(R, np.float64)
+    rc = _load().oracle_topp_rows(_p(qp, ctypes.c_double), _p(k, ctypes.c_double), N, D, pq, int(causal), scale,
+                                  float(p), _p(rows, ctypes.c_int64), R, _p(counts, ctypes.c_int64),
+                                  _p(idx, ctypes.c_int32), N, _p(mass, ctypes.c_double))
+    if rc:
+        raise ValueError(f"oracle_topp_rows: bad arguments (rc={rc})")
+    offsets = np.zeros(R + 1, np.int64)
+    np.cumsum(counts, out=offsets[1:])
+    indices = (np.concatenate([idx[r, :counts[r]] for r in range(R)]) if R else np.zeros(0)).astype(np.int32)
+    return (offsets, indices, mass) if detail else (offsets, indices)
 
 
 # ---------------------------------------------------------------------- attention

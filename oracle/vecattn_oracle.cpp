@@ -14,6 +14,7 @@
 //   Eq. 1 dense attention ............ P:54-68 (Sec. 2.1)
 //   Eq. 2 query pooling ............... P:187-194 (Sec. 3.1.1), Alg. 1 line P:770
 //   Eq. 3 minS filter ................. P:218-232 (Sec. 3.1.2)
+//   topP naive filter ................. P:203-216 (Sec. 3.1.1-3.1.2)
 //   TilingSelect / G_K running max .... P:268-278, P:290-307 (Sec. 3.1.3)
 //   Alg. 1 important-vector selection . P:755-850 (App. D.1)
 //   Eq. 5 vector-sparse attention ..... P:309-341 (Sec. 3.2), Alg. 2
@@ -220,6 +221,55 @@ int oracle_select_rows(const double* qp, const double* k, int64_t N, int64_t D, 
         }
         if (mode == 0) std::sort(out, out + c);   // already ascending; canonical form (R9)
         counts[r] = c;
+    }
+    return 0;
+}
+
+// topP ("nucleus") selection of the NAIVE approach: the estimated
+// attention map A_p[i,:] = softmax_j(s_ij) over the visible keys (softmax of
+// Eq. 1 applied to the pooled scores), then the smallest prefix of keys sorted by
+// descending probability (ties -> lowest index, reading R12) whose cumulative mass is
+// >= p; keys of zero probability (fp64 underflow) are never taken, so p >= 1 returns
+// every nonzero-probability key.  Causal: keys j > L_i are excluded first (R5).
+// Outputs per requested row r: counts[r], ascending indices in idx[r*idx_stride ...],
+// and optionally mass[r] = the selected cumulative probability.  Returns 0 / 1 (bad args).
+int oracle_topp_rows(const double* qp, const double* k, int64_t N, int64_t D, int32_t pq,
+                     int32_t causal, double scale, double p, const int64_t* rows, int64_t nrows,
+                     int64_t* counts, int32_t* idx, int64_t idx_stride, double* mass) {
+    if (!qp || !k || !rows || !counts || !idx || N < 1 || D < 1 || pq < 1 || idx_stride < N ||
+        !(p > 0.0 && p <= 1.0))
+        return 1;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t r = 0; r < nrows; ++r) {
+        const int64_t i = rows[r];
+        const int64_t vend = visible_end(i, N, pq, causal);
+        std::vector<double> s(vend), a(vend);
+        for (int64_t j = 0; j < vend; ++j) s[j] = scale * dot(qp + i * D, k + j * D, D);
+        double m = NEG_INF;                                          // softmax: max ...
+        for (int64_t j = 0; j < vend; ++j) m = std::max(m, s[j]);
+        double z = 0.0;                                              // ... normaliser ...
+        for (int64_t j = 0; j < vend; ++j) z += std::exp(s[j] - m);
+        for (int64_t j = 0; j < vend; ++j) a[j] = std::exp(s[j] - m) / z;   // ... A_p[i, j]
+        std::vector<int64_t> order(vend);
+        for (int64_t j = 0; j < vend; ++j) order[j] = j;
+        std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) {
+            if (a[x] != a[y]) return a[x] > a[y];                     // descending probability
+            return x < y;                                            // ties -> lowest index (R12)
+        });
+        std::vector<int32_t> sel;
+        double cum = 0.0;
+        for (int64_t t = 0; t < vend; ++t) {                         // smallest prefix with mass >= p
+            const int64_t j = order[t];
+            if (a[j] == 0.0) break;                                  // zero probability: never taken
+            sel.push_back((int32_t)j);
+            cum += a[j];
+            if (cum >= p) break;
+        }
+        std::sort(sel.begin(), sel.end());
+        int32_t* out = idx + r * idx_stride;
+        for (size_t t = 0; t < sel.size(); ++t) out[t] = sel[t];
+        counts[r] = (int64_t)sel.size();
+        if (mass) mass[r] = cum;
     }
     return 0;
 }
