@@ -145,6 +145,29 @@ VECATTN_API size_t vecattn_dense_workspace_bytes(const vecattn_problem_t* p);
 VECATTN_API vecattn_status_t vecattn_dense_fwd(const vecattn_problem_t* p, const void* q, const void* k, const void* v,
                                    void* o, float* lse, void* ws, size_t ws_bytes, vecattn_stream_t stream);
 
+/* ------------------------------------------------ naive selection baselines */
+
+/* The paper's NAIVE materialise-then-filter selection (Fig. 5), the
+ * comparison baseline for the fused vecattn_select.  The pooled
+ * score map S_p = Q_p K^T (fp32, [B*Hq*N_p, N]) is written to the workspace in HBM and
+ * filtered row by row:
+ *   VECATTN_NAIVE_MINS  Eq. 3 with the global row max: the same index sets as
+ *                       vecattn_select(VECATTN_SEL_MINS_EXACT) with the same alpha.
+ *   VECATTN_NAIVE_TOPP  topP: per row softmax(scale * s) over the
+ *                       visible keys, keys sorted by descending probability (ties -> lowest
+ *                       index), the smallest prefix whose cumulative mass is >= top_p; keys
+ *                       of zero (fp32) probability are never taken.
+ * Arguments, CSR layout, capacity protocol and causal rule as vecattn_select (indices may be
+ * NULL with cap = 0 for counts only).  alpha >= 0 (MINS), 0 < top_p <= 1 (TOPP); pq in {64,
+ * 128}.  The workspace (vecattn_select_naive_workspace_bytes) holds the 4*R*N-byte score map
+ * and, for TOPP, sort buffers for up to 2^29 keys at a time; errors as vecattn_select.      */
+typedef enum { VECATTN_NAIVE_MINS = 0, VECATTN_NAIVE_TOPP = 1 } vecattn_naive_mode_t;
+VECATTN_API size_t vecattn_select_naive_workspace_bytes(const vecattn_problem_t* p, int32_t pq, int32_t mode);
+VECATTN_API vecattn_status_t vecattn_select_naive(const vecattn_problem_t* p, int32_t pq, int32_t mode, float alpha,
+                                                  float top_p, const void* q, const void* k, int64_t* offsets,
+                                                  int32_t* indices, int64_t cap, int64_t* d_nnz, void* ws,
+                                                  size_t ws_bytes, vecattn_stream_t stream);
+
 /* ----------------------------------------------------------- diagnostics */
 
 /* Test hook: writes d_bad[0] = number of CSR rows violating ascending/unique/range/

@@ -293,6 +293,122 @@ vecattn_status_t vecattn_kernel_timing_last(float* select_ms, float* plan_ms, fl
     return VECATTN_OK;
 }
 
+// ------------------------------------------------------------ naive selection baselines
+namespace {
+struct NaiveWs {
+    float* scores;
+    float* rmax;
+    double* rz;
+    float* skeys;
+    int32_t* vals_in;
+    int32_t* vals_out;
+    int64_t* seg_begin;
+    int64_t* seg_end;
+    void* temp;
+    size_t temp_bytes;
+    size_t total;
+};
+NaiveWs carve_naive(const vecattn_problem_t* p, int32_t pq, int32_t mode, void* base) {
+    const int64_t R = p->B * p->Hq * n_pooled(p, pq), N = p->N;
+    uint8_t* b = static_cast<uint8_t*>(base);
+    NaiveWs w;
+    memset(&w, 0, sizeof(w));
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        uint8_t* x = b ? b + off : nullptr;
+        off += align_up(bytes);
+        return x;
+    };
+    w.scores = reinterpret_cast<float*>(take((size_t)R * N * 4));
+    w.rmax = reinterpret_cast<float*>(take((size_t)R * 4));
+    w.rz = reinterpret_cast<double*>(take((size_t)R * 8));
+    if (mode == VECATTN_NAIVE_TOPP) {
+        const int64_t B = va::naive_topp_batch_rows(R, N);
+        w.skeys = reinterpret_cast<float*>(take((size_t)B * N * 4));
+        w.vals_in = reinterpret_cast<int32_t*>(take((size_t)B * N * 4));
+        w.vals_out = reinterpret_cast<int32_t*>(take((size_t)B * N * 4));
+        w.seg_begin = reinterpret_cast<int64_t*>(take((size_t)B * 8));
+        w.seg_end = reinterpret_cast<int64_t*>(take((size_t)B * 8));
+        w.temp_bytes = va::naive_topp_sort_temp_bytes(B, N);
+        w.temp = take(w.temp_bytes);
+    }
+    w.total = off;
+    return w;
+}
+}  // namespace
+
+size_t vecattn_select_naive_workspace_bytes(const vecattn_problem_t* p, int32_t pq, int32_t mode) {
+    if (check_problem(p) != VECATTN_OK || (pq != 64 && pq != 128) ||
+        (mode != VECATTN_NAIVE_MINS && mode != VECATTN_NAIVE_TOPP))
+        return 0;
+    return carve_select(p, pq, nullptr).total + carve_naive(p, pq, mode, nullptr).total + kAlign;
+}
+
+vecattn_status_t vecattn_select_naive(const vecattn_problem_t* p, int32_t pq, int32_t mode, float alpha, float top_p,
+                                      const void* q, const void* k, int64_t* offsets, int32_t* indices, int64_t cap,
+                                      int64_t* d_nnz, void* ws, size_t ws_bytes, vecattn_stream_t stream) {
+    vecattn_status_t st = check_problem(p);
+    if (st != VECATTN_OK) return st;
+    if ((pq != 64 && pq != 128) || (mode != VECATTN_NAIVE_MINS && mode != VECATTN_NAIVE_TOPP) || !q || !k ||
+        !offsets || !d_nnz || cap < 0 || (cap > 0 && !indices))
+        return VECATTN_ERR_INVALID_ARGUMENT;
+    if (mode == VECATTN_NAIVE_MINS && !(alpha >= 0.f && alpha < INFINITY)) return VECATTN_ERR_INVALID_ARGUMENT;
+    if (mode == VECATTN_NAIVE_TOPP && !(top_p > 0.f && top_p <= 1.f)) return VECATTN_ERR_INVALID_ARGUMENT;
+    if (!aligned16(q) || !aligned16(k)) return VECATTN_ERR_SHAPE;
+    const size_t need = vecattn_select_naive_workspace_bytes(p, pq, mode);
+    if (!ws || ws_bytes < need) return VECATTN_ERR_WORKSPACE;
+    if (!aligned16(ws)) return VECATTN_ERR_SHAPE;
+    cudaStream_t cs = (cudaStream_t)stream;
+    const SelectWs w = carve_select(p, pq, ws);
+    const NaiveWs nw = carve_naive(p, pq, mode, static_cast<uint8_t*>(ws) + w.total);
+    vecattn_select_params_t s;
+    memset(&s, 0, sizeof(s));
+    s.mode = VECATTN_SEL_MINS_EXACT;
+    s.pq = pq;
+    s.bk = 16;
+    s.gk = 1;
+    s.alpha = alpha;
+    SelectParams* sp = new SelectParams;
+    st = fill_select_params(p, &s, pq, k, w, *sp);
+    if (st == VECATTN_OK) st = set_k_map(p, k, 256, *sp);
+    if (st != VECATTN_OK) { delete sp; return st; }
+    sp->scores_out = nw.scores;
+    plan_segments(p, &s, va::EPI_SCORES, *sp);
+    const float scale = eff_scale(p);
+    const float alpha_raw = sp->alpha_raw[0];  // alpha / scale, exactly as the fused MINS_EXACT
+    const int64_t R = sp->BH * sp->Np;
+    if (g_timing.enabled) {
+        tbegin(true, true);
+        g_timing.has_attn = false;
+    }
+    tmark(0, cs);
+    cudaError_t e = va::launch_pool(q, w.qp, sp->BH, p->N, p->D, pq, cs);
+    if (e == cudaSuccess) e = va::launch_select(*sp, va::EPI_SCORES, (int)p->D, cs);  // S_p -> HBM
+    tmark(1, cs);
+    const float sl2 = scale * 1.4426950408889634f;
+    if (e == cudaSuccess)
+        e = va::launch_naive_row_stats(nw.scores, R, sp->Np, p->N, pq, p->causal ? 1 : 0, sl2,
+                                       mode == VECATTN_NAIVE_TOPP ? 1 : 0, nw.rmax, nw.rz, cs);
+    if (e == cudaSuccess) {
+        if (mode == VECATTN_NAIVE_MINS)
+            e = va::launch_naive_mins(nw.scores, R, sp->Np, p->N, pq, p->causal ? 1 : 0, nw.rmax, alpha_raw, w.bitmask,
+                                      sp->words_per_row, w.counts, cs);
+        else
+            e = va::launch_naive_topp(nw.scores, R, sp->Np, p->N, pq, p->causal ? 1 : 0, sl2, top_p, nw.rmax, nw.rz,
+                                      nw.skeys, nw.vals_in, nw.vals_out, nw.seg_begin, nw.seg_end, nw.temp,
+                                      nw.temp_bytes, w.bitmask, sp->words_per_row, w.counts, cs);
+    }
+    if (e == cudaSuccess) e = va::launch_scan(w.counts, R, offsets, d_nnz, cs);
+    if (e == cudaSuccess && indices && cap > 0)
+        e = va::launch_emit(w.bitmask, sp->words_per_row, offsets, d_nnz, cap, indices, sp->BH, sp->Np, p->N, pq,
+                            p->causal ? 1 : 0, cs);
+    tmark(2, cs);
+    tmark(3, cs);
+    delete sp;
+    return cuda_status(e);
+}
+
+
 const char* vecattn_last_cuda_error(void) { return cudaGetErrorString(g_last_cuda_error); }
 
 const char* vecattn_status_string(vecattn_status_t s) {

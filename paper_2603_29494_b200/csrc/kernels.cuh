@@ -64,6 +64,21 @@ cudaError_t launch_plan(const uint32_t* bitmask, int64_t words_per_row, const in
                         int64_t wl_cap, uint32_t* wl, int32_t* wl_len, int64_t BH, int64_t Np, int64_t N, int32_t pq,
                         int32_t causal, cudaStream_t st);
 
+// ------------------------------------------------------------- naive baselines (naive.cu)
+// Materialise-then-filter selection (Fig. 5): row statistics, minS filter, topP
+// (segmented sort + cumulative-mass cut), all on the raw fp32 score map [R, N].
+cudaError_t launch_naive_row_stats(const float* scores, int64_t R, int64_t Np, int64_t N, int32_t pq, int32_t causal,
+                                   float sl2, int want_z, float* rmax, double* rz, cudaStream_t st);
+cudaError_t launch_naive_mins(const float* scores, int64_t R, int64_t Np, int64_t N, int32_t pq, int32_t causal,
+                              const float* rmax, float alpha_raw, uint32_t* bitmask, int64_t words_per_row,
+                              unsigned long long* counts, cudaStream_t st);
+int64_t naive_topp_batch_rows(int64_t R, int64_t N);
+size_t naive_topp_sort_temp_bytes(int64_t batch_rows, int64_t N);
+cudaError_t launch_naive_topp(const float* scores, int64_t R, int64_t Np, int64_t N, int32_t pq, int32_t causal,
+                              float sl2, float top_p, const float* rmax, const double* rz, float* skeys, int32_t* vals_in,
+                              int32_t* vals_out, int64_t* seg_begin, int64_t* seg_end, void* temp, size_t temp_bytes,
+                              uint32_t* bitmask, int64_t words_per_row, unsigned long long* counts, cudaStream_t st);
+
 // ----------------------------------------------------------------------- attention
 struct AttnParams {
     alignas(64) CUtensorMap tm_q;  // 3-D {D, N, B*Hq}, box {64, 128, 1}

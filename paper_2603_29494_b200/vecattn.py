@@ -71,6 +71,9 @@ def load(path: str = LIB_PATH):
         "vecattn_last_cuda_error": (ctypes.c_char_p, []),
         "vecattn_abi_version": (i32, []),
         "vecattn_kernel_timing": (i32, [i32]),
+        "vecattn_select_naive_workspace_bytes": (sz, [prob, i32, i32]),
+        "vecattn_select_naive": (i32, [prob, i32, i32, ctypes.c_float, ctypes.c_float, vp, vp, vp, vp, i64, vp, vp,
+                                       sz, vp]),
         "vecattn_kernel_timing_last": (i32, [P(ctypes.c_float), P(ctypes.c_float), P(ctypes.c_float)]),
     }
     for name, (res, args) in sig.items():
@@ -85,7 +88,47 @@ EXPORTED = ["vecattn_pool", "vecattn_select_workspace_bytes", "vecattn_select", 
             "vecattn_sparse_fwd", "vecattn_dense_workspace_bytes", "vecattn_dense_fwd",
             "vecattn_forward_workspace_bytes", "vecattn_forward",
             "vecattn_validate_selection", "vecattn_debug_scores", "vecattn_status_string", "vecattn_last_cuda_error",
-            "vecattn_abi_version", "vecattn_kernel_timing", "vecattn_kernel_timing_last"]
+            "vecattn_abi_version", "vecattn_kernel_timing", "vecattn_kernel_timing_last",
+            "vecattn_select_naive_workspace_bytes", "vecattn_select_naive"]
+
+NAIVE_MINS = 0
+NAIVE_TOPP = 1
+NAIVE_MODES = {"mins": NAIVE_MINS, "topp": NAIVE_TOPP}
+
+
+def select_naive_workspace_bytes(pr: Problem, pq: int, mode: str) -> int:
+    return int(load().vecattn_select_naive_workspace_bytes(ctypes.byref(pr), pq, NAIVE_MODES[mode]))
+
+
+def select_naive_into(q, k, mode: str, offsets, indices, cap: int, d_nnz, ws: torch.Tensor, *, pq: int = 64,
+                      alpha: float = 0.0, top_p: float = 0.9, causal: bool = False, scale=None, stream=None):
+    """Raw vecattn_select_naive call (materialise-then-filter baseline) into caller buffers."""
+    lib = load()
+    _dev_check(q, k, offsets, indices, d_nnz)
+    pr = problem(q, k, causal, scale)
+    rc = lib.vecattn_select_naive(ctypes.byref(pr), int(pq), NAIVE_MODES[mode], float(alpha), float(top_p), _ptr(q),
+                                  _ptr(k), _ptr(offsets), _ptr(indices), int(cap), _ptr(d_nnz), _ptr(ws), ws.numel(),
+                                  _stream(stream))
+    _check("vecattn_select_naive", rc)
+
+
+def select_naive(q, k, mode: str, *, pq: int = 64, alpha: float = 0.0, top_p: float = 0.9, causal: bool = False,
+                 scale=None, ws: "Workspace | None" = None, stream=None):
+    """Naive selection baseline with the capacity protocol: returns (offsets int64, indices int32)."""
+    B, H, N, D = q.shape
+    Np = (N + pq - 1) // pq
+    pr = problem(q, k, causal, scale)
+    ws = ws or Workspace(q.device)
+    wbuf = ws.get(select_naive_workspace_bytes(pr, pq, mode))
+    offsets = torch.empty(B * H * Np + 1, dtype=torch.int64, device=q.device)
+    d_nnz = torch.empty(1, dtype=torch.int64, device=q.device)
+    select_naive_into(q, k, mode, offsets, None, 0, d_nnz, wbuf, pq=pq, alpha=alpha, top_p=top_p, causal=causal,
+                      scale=scale, stream=stream)
+    cap = int(d_nnz.item())
+    indices = torch.empty(max(cap, 1), dtype=torch.int32, device=q.device)
+    select_naive_into(q, k, mode, offsets, indices, cap, d_nnz, wbuf, pq=pq, alpha=alpha, top_p=top_p,
+                      causal=causal, scale=scale, stream=stream)
+    return offsets, indices[:cap]
 
 
 def kernel_timing(enable: bool) -> None:
