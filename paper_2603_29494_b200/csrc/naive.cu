@@ -54,22 +54,36 @@ VA_DEV double block_sum(double v, double* sh) {
 
 // Row statistics of the materialised map: max of the raw accumulators over the visible
 // keys, and (topP) Z = sum_j exp2((acc_j - max) * scale*log2e) (fp32 terms, fp64 sum).
+// Rows are read with 16-B loads when N % 4 == 0 (the visible extent is then a multiple of 4
+// except for a ragged N, handled by the scalar tail).
 __global__ void __launch_bounds__(kRowThreads) row_stats_kernel(const float* __restrict__ scores, int64_t R,
                                                                  int64_t Np, int64_t N, int32_t pq, int32_t causal,
                                                                  float sl2, int32_t want_z, float* __restrict__ rmax,
                                                                  double* __restrict__ rz) {
     __shared__ float shf[32];
     __shared__ double shd[32];
+    const bool vec = (N & 3) == 0;
     for (int64_t row = blockIdx.x; row < R; row += gridDim.x) {
         const int64_t vend = vis_end(row, Np, N, pq, causal);
+        const int64_t v4 = vec ? vend / 4 : 0;
         const float* s = scores + row * N;
+        const float4* s4 = reinterpret_cast<const float4*>(s);
         float m = -INFINITY;
-        for (int64_t j = threadIdx.x; j < vend; j += kRowThreads) m = fmaxf(m, __ldg(s + j));
+        for (int64_t j = threadIdx.x; j < v4; j += kRowThreads) {
+            const float4 x = __ldg(s4 + j);
+            m = fmaxf(fmaxf(m, fmaxf(x.x, x.y)), fmaxf(x.z, x.w));
+        }
+        for (int64_t j = 4 * v4 + threadIdx.x; j < vend; j += kRowThreads) m = fmaxf(m, __ldg(s + j));
         m = block_max(m, shf);
         if (threadIdx.x == 0) rmax[row] = m;
         if (want_z) {
             double z = 0.0;
-            for (int64_t j = threadIdx.x; j < vend; j += kRowThreads) z += (double)exp2f((__ldg(s + j) - m) * sl2);
+            for (int64_t j = threadIdx.x; j < v4; j += kRowThreads) {
+                const float4 x = __ldg(s4 + j);
+                z += (double)(exp2f((x.x - m) * sl2) + exp2f((x.y - m) * sl2)) +
+                     (double)(exp2f((x.z - m) * sl2) + exp2f((x.w - m) * sl2));
+            }
+            for (int64_t j = 4 * v4 + threadIdx.x; j < vend; j += kRowThreads) z += (double)exp2f((__ldg(s + j) - m) * sl2);
             z = block_sum(z, shd);
             if (threadIdx.x == 0) rz[row] = z;
         }
@@ -77,6 +91,7 @@ __global__ void __launch_bounds__(kRowThreads) row_stats_kernel(const float* __r
 }
 
 // minS filter (Eq. 3): bit j of row r set iff acc_rj >= max_r - alpha_raw (alpha/scale).
+// A lane tests 4 consecutive keys (one 16-B load); 8 lanes OR their nibbles into a word.
 __global__ void __launch_bounds__(kRowThreads) mins_filter_kernel(const float* __restrict__ scores, int64_t R,
                                                                    int64_t Np, int64_t N, int32_t pq, int32_t causal,
                                                                    const float* __restrict__ rmax, float alpha_raw,
@@ -84,22 +99,34 @@ __global__ void __launch_bounds__(kRowThreads) mins_filter_kernel(const float* _
                                                                    int64_t words_per_row,
                                                                    unsigned long long* __restrict__ counts) {
     __shared__ double shd[32];
+    const int lane = threadIdx.x & 31;
+    const bool vec = (N & 3) == 0;
     for (int64_t row = blockIdx.x; row < R; row += gridDim.x) {
         const int64_t vend = vis_end(row, Np, N, pq, causal);
         const float thr = rmax[row] - alpha_raw;
         const float* s = scores + row * N;
         uint32_t* bm = bitmask + row * words_per_row;
         double cnt = 0.0;
-        for (int64_t w = threadIdx.x; w < words_per_row; w += kRowThreads) {
-            uint32_t word = 0;
-            const int64_t j0 = w * 32;
+        // words_per_row * 8 quads per row; every lane of the block walks the quads in order
+        for (int64_t qd0 = 0; qd0 < words_per_row * 8; qd0 += kRowThreads) {
+            const int64_t qd = qd0 + threadIdx.x;
+            const int64_t j0 = 4 * qd;
+            uint32_t nib = 0;
             if (j0 < vend) {
-#pragma unroll 8
-                for (int b = 0; b < 32; ++b)
-                    if (j0 + b < vend && __ldg(s + j0 + b) >= thr) word |= 1u << b;
+                if (vec && j0 + 4 <= vend) {
+                    const float4 x = __ldg(reinterpret_cast<const float4*>(s + j0));
+                    nib = (x.x >= thr ? 1u : 0u) | (x.y >= thr ? 2u : 0u) | (x.z >= thr ? 4u : 0u) | (x.w >= thr ? 8u : 0u);
+                } else {
+                    for (int b = 0; b < 4; ++b)
+                        if (j0 + b < vend && __ldg(s + j0 + b) >= thr) nib |= 1u << b;
+                }
             }
-            bm[w] = word;
-            cnt += __popc(word);
+            uint32_t word = nib << (4 * (lane & 7));
+            word |= __shfl_xor_sync(0xffffffffu, word, 1);
+            word |= __shfl_xor_sync(0xffffffffu, word, 2);
+            word |= __shfl_xor_sync(0xffffffffu, word, 4);
+            if ((lane & 7) == 0 && qd / 8 < words_per_row) bm[qd / 8] = word;
+            cnt += __popc(nib);
         }
         cnt = block_sum(cnt, shd);
         if (threadIdx.x == 0) counts[row] = (unsigned long long)cnt;

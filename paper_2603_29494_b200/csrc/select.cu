@@ -220,9 +220,16 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
 
                 if constexpr (EPI == EPI_SCORES) {
                     if (row_ok) {
+                        float* dst = p.scores_out + grow * p.N + kc;
+                        if ((p.N & 3) == 0 && kc + 64 <= p.N) {  // 16-B stores (row-contiguous)
 #pragma unroll
-                        for (int j = 0; j < 64; ++j)
-                            if (kc + j < p.N) p.scores_out[grow * p.N + kc + j] = v[j];
+                            for (int j = 0; j < 64; j += 4)
+                                *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 64; ++j)
+                                if (kc + j < p.N) dst[j] = v[j];
+                        }
                     }
                 } else if constexpr (EPI == EPI_ALG1) {
                     if (nvis < 64) {
