@@ -16,15 +16,20 @@
 //    still computes exactly Eq. 5 over its own Idx(i).
 //  * Membership masking runs on the tensor core: S = [Q | onehot(block)] [K | bias]^T
 //    with one extra K=16 MMA step, bias = 0 (member) or -2^100 (non-member).
-//  * 64-key chunks, 4-stage K and V rings; K/V rows gathered with TMA tile::gather4
-//    (4 rows x 128 B per instruction) by 2 K-loader and 2 V-loader warps (32 keys
-//    each, plan entries prefetched one chunk ahead); dense mode uses 64x64 TMA tiles.
-//  * MMA warp: S_t = Q_t K^T (M=128, N=64) into double-buffered TMEM per tile, issued
-//    one chunk ahead; O_t += P_t V with A = P_t from TMEM (bf16, written by the softmax
-//    over S_t) and B = V (MN-major) from shared memory.
-//  * Softmax warpgroup t (thread = query row = TMEM lane): row max in a first TMEM
-//    pass, lazy rescale (threshold 2^8, warp-voted because tcgen05.ld/st are
-//    warp-collective), exp2 with f32x2 FMA/ADD in a second pass.
+//  * 128-key chunks: S_t = Q_t K^T is one M=128 N=128 MMA per K-step (an N=64 MMA with A
+//    from shared memory runs at 43% of peak, N=128 at 60%; profiles/ubench_r01.md).
+//    TMEM holds O_0, O_1 (128 columns each) and a single S_t buffer per tile (128 columns,
+//    P_t written as bf16 over its first 64): per tile the tensor core runs
+//    S_t(c) -> [softmax_t] -> PV_t(c) -> S_t(next), and the two tiles ping-pong so each
+//    tile's softmax overlaps the other tile's MMAs.  S_t(next) is issued after PV_t(c) (the
+//    tensor pipe is in order), so SFULL_t also certifies that O_t is stable for a rescale.
+//  * Two ring stages of 128 keys; 4 loader warps, warp (stage s, half h) owns keys
+//    [64h, 64h+64) of every chunk on stage s: K_ext rows + K gathers, then the keys for the
+//    causal mask + V gathers (TMA tile::gather4, 4 rows x 128 B each); dense mode uses
+//    128x64 TMA tiles.
+//  * Softmax warpgroup t (thread = query row = TMEM lane): row max over the 128 columns in
+//    a first TMEM pass, lazy rescale (threshold 2^8, warp-voted), then exp2 (f32x2 FMA; 1 of
+//    4 column groups on the FMA pipe by polynomial) and bf16 P in a second pass.
 //  * Persistent CTAs, dynamic atomic scheduler, items head-major (one head's K/V
 //    stays L2-resident), causal items longest-first.
 // Degenerate rows (no visible selected key; reading R6): O_r = V_r,
@@ -38,41 +43,51 @@ namespace va {
 
 namespace {
 
-constexpr int kThreads = 448;  // w0 sched+Q, w1 MMA, w2-5 softmax tile 0, w6-9 softmax tile 1, w10-13 loaders
+// Warpgroups (setmaxnreg works per warpgroup): WG0 = w0 scheduler + Q loads, w1 MMA issuer,
+// w2-3 loaders; WG1 = w4-7 softmax tile 0; WG2 = w8-11 softmax tile 1; WG3 = w12-13 loaders
+// (w14-15 idle).  The softmax warpgroups raise their register budget to 192 so a thread
+// holds its whole 128-column S row; the others drop to 64 (65536 registers in total).
+constexpr int kThreads = 512;
 constexpr int kLoadWarps = 4;
-constexpr int kFirstLoadWarp = 10;
+constexpr int kSoftmaxRegs = 192, kOtherRegs = 64;
+VA_DEV int loader_index(uint32_t w) { return w == 2 ? 0 : w == 3 ? 1 : w == 12 ? 2 : w == 13 ? 3 : -1; }
+VA_DEV void setmaxnreg_inc192() { asm volatile("setmaxnreg.inc.sync.aligned.u32 192;"); }
+VA_DEV void setmaxnreg_dec64() { asm volatile("setmaxnreg.dec.sync.aligned.u32 64;"); }
 constexpr int kSoftmaxThreads = 256;
-constexpr int kChunk = 64;                  // keys per K/V chunk
+constexpr int kChunk = 128;                 // keys per K/V chunk
 constexpr uint32_t kKeyMask = 0x0FFFFFFFu;  // entry = key | membership << 28
 constexpr uint32_t kPad = 0x0FFFFFFFu;      // meta key for padding lanes (sorts last)
+constexpr uint32_t kNegInfBits = 0xff800000u;
+constexpr int kPolyEvery = 4;  // 1 of every kPolyEvery groups of 4 columns takes exp2 on the FMA pipe
 
 template <int D>
 struct AttnCfg {
-    static constexpr int kStages = D == 128 ? 4 : 8;
+    static constexpr int kStages = 2;                      // == kLoadWarps / 2 (stage ownership)
     static constexpr int kCB = D / 64;
     static constexpr int kQTileBytes = kCB * 128 * 128;   // 128 rows x D bf16
-    static constexpr int kKVBytes = kCB * kChunk * 128;    // 64 keys x D bf16
+    static constexpr int kKVBytes = kCB * kChunk * 128;    // 128 keys x D bf16
     static constexpr int kOffQ = 0;                        // two Q tiles
     static constexpr int kOffK = 2 * kQTileBytes;
     static constexpr int kOffV = kOffK + kStages * kKVBytes;
     static constexpr int kOffMeta = kOffV + kStages * kKVBytes;
     static constexpr int kOffQx = (kOffMeta + kStages * kChunk * 4 + 1023) / 1024 * 1024;  // Q_ext [2][128 x 16]
-    static constexpr int kOffKx = kOffQx + 2 * 128 * 16 * 2;                               // K_ext [S][64 x 16]
+    static constexpr int kOffKx = kOffQx + 2 * 128 * 16 * 2;                               // K_ext [S][128 x 16]
     static constexpr int kOffBar = kOffKx + kStages * kChunk * 16 * 2;
     static constexpr int B_QFULL = 0, B_QEMPTY = 1, B_KFULL = 2, B_KEMPTY = B_KFULL + kStages,
                          B_VFULL = B_KEMPTY + kStages, B_VEMPTY = B_VFULL + kStages,
-                         B_MFULL = B_VEMPTY + kStages, B_SFULL = B_MFULL + kStages /* [2 tiles][2 bufs] */,
-                         B_PFULL = B_SFULL + 4, B_ODONE = B_PFULL + 4, B_OEMPTY = B_ODONE + 2,
-                         B_IFULL = B_OEMPTY + 2, B_IEMPTY = B_IFULL + 2, B_OFIN = B_IEMPTY + 2, kNumBars = B_OFIN + 2;
+                         B_MFULL = B_VEMPTY + kStages, B_SFULL = B_MFULL + kStages /* [2 tiles] */,
+                         B_PFULL = B_SFULL + 2, B_OEMPTY = B_PFULL + 2, B_OFIN = B_OEMPTY + 2,
+                         B_IFULL = B_OFIN + 1, B_IEMPTY = B_IFULL + 2, kNumBars = B_IEMPTY + 2;
     static constexpr int kOffItem = kOffBar + kNumBars * 8;
     static constexpr int kSmem = kOffItem + 16;
-    // TMEM: O_t at 128t (D cols); S[t][b] at 256 + 128t + 64b (64 cols; P over its first 32)
+    // TMEM: O_t at 128t (D cols); S_t at 256 + 128t (128 cols; P_t over its first 64)
     static constexpr uint32_t kTmemCols = 512;
     static constexpr uint32_t kIdescS = make_idesc_bf16(128, kChunk, 0, 0);
     static constexpr uint32_t kIdescPV = make_idesc_bf16(128, D, 0, 1);
 };
 
-VA_DEV uint32_t s_col(int t, int b) { return 256u + 128u * t + 64u * b; }
+VA_DEV uint32_t o_col(int t) { return 128u * t; }
+VA_DEV uint32_t s_col(int t) { return 256u + 128u * t; }
 
 // Debug timeline (p.trace != null): CTA 0 records clock64() per chunk and event kind
 // (0 K issue, 1 V issue, 2 K landed, 3 V landed, 4/5 PV0/PV1 issued, 6/7 S0 ready/P0 done,
@@ -164,7 +179,31 @@ VA_DEV Chunk chunk_info(const Item& I, int j) {
     }
 }
 
-VA_DEV uint32_t prefix_mask(int64_t nb) { return nb >= 32 ? 0xffffffffu : (nb <= 0 ? 0u : ((1u << nb) - 1u)); }
+// First chunk index > j that tile t computes (n_chunks if none).
+template <bool GATHER>
+VA_DEV int next_chunk(const Item& I, int t, int j) {
+    if constexpr (!GATHER) {
+        return j + 1;
+    } else {
+        const int n = I.n_chunks;
+        const int mt = t == 0 ? I.n0 : I.n1;
+        const int m = min(I.n0, I.n1);
+        int x = j + 1;
+        if (x < I.nb) return x;
+        if (mt == 0) return n;
+        // own chunks of tile t after the shared segment: interleaved k = 2q + t (q < m), then
+        // (if t owns the longer list) the tail k >= 2m
+        const int k = x - I.nb;
+        if (k < 2 * m) {
+            const int kk = ((k & 1) == t) ? k : k + 1;
+            if (kk < 2 * m) return I.nb + kk;
+            // past the interleave: the tail belongs to tile t only if its list is the longer
+        }
+        const bool tail_owner = (t == 0) ? (I.n0 > I.n1) : (I.n1 >= I.n0);
+        if (!tail_owner || mt == m) return n;
+        return max(x, I.nb + 2 * m);
+    }
+}
 
 }  // namespace
 
@@ -190,29 +229,26 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         mbar_init(&bars[C::B_QFULL], 1);
         mbar_init(&bars[C::B_QEMPTY], 1);
         for (int s = 0; s < S_; ++s) {
-            mbar_init(&bars[C::B_KFULL + s], 1);
+            mbar_init(&bars[C::B_KFULL + s], GATHER ? 2 : 1);  // two K half-warps
             mbar_init(&bars[C::B_KEMPTY + s], 1);
-            mbar_init(&bars[C::B_VFULL + s], 1);
+            mbar_init(&bars[C::B_VFULL + s], GATHER ? 2 : 1);
             mbar_init(&bars[C::B_VEMPTY + s], 1);
-            mbar_init(&bars[C::B_MFULL + s], 1);
-        }
-        for (int x = 0; x < 4; ++x) {
-            mbar_init(&bars[C::B_SFULL + x], 1);
-            mbar_init(&bars[C::B_PFULL + x], 128);
+            mbar_init(&bars[C::B_MFULL + s], 2);
         }
         for (int t = 0; t < 2; ++t) {
-            mbar_init(&bars[C::B_ODONE + t], 1);
+            mbar_init(&bars[C::B_SFULL + t], 1);
+            mbar_init(&bars[C::B_PFULL + t], 128);
             mbar_init(&bars[C::B_OEMPTY + t], 128);
             mbar_init(&bars[C::B_IFULL + t], 1);
             mbar_init(&bars[C::B_IEMPTY + t], 1 + kSoftmaxThreads + kLoadWarps);
-            mbar_init(&bars[C::B_OFIN + t], 1);
         }
+        mbar_init(&bars[C::B_OFIN], 1);
         fence_barrier_init();
     }
     if constexpr (GATHER) {
         // Membership masking on the tensor core: S = [Q | E] [K | F]^T with E = one-hot of the
         // row's block (Q_ext, constant per row position) and F[j][b] = 0 if key j is in block
-        // b's index set else -2^100 (K_ext, written per chunk by the K loaders).  Members get
+        // b's index set else -2^100 (K_ext, written per chunk by the loaders).  Members get
         // +0 exactly; non-members a score of -2^100 whose exp2 underflows to 0.
         uint16_t* qx = reinterpret_cast<uint16_t*>(smem + C::kOffQx);
         for (int x = threadIdx.x; x < 2 * 128 * 16; x += kThreads) {
@@ -229,7 +265,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const bool softmax_wg = warp >= 4 && warp < 12;
 
+    if (!softmax_wg) {
+    setmaxnreg_dec64();  // whole warpgroups WG0 / WG3 (setmaxnreg is warpgroup-collective)
     if (warp == 0) {
         // ======================================== scheduler: dynamic items + Q tile loads
         if (lane == 0) {
@@ -263,20 +302,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             }
             ++qi;
         }
-    } else if (warp >= kFirstLoadWarp) {
+    } else if (loader_index(warp) >= 0) {
         // ======================================== K/V loaders (4 warps)
-        // Warp g owns every chunk c = g (mod 4): K and V of all 64 keys.  A warp's TMA issue
-        // rate is bound by a fixed per-iteration cost plus ~70 clk per gather4 (uniform-register
-        // setup), so whole chunks per warp (fewer iterations each) beat splitting every chunk
-        // across warps (scripts/ubench_gather.cu).  Stage s = c % S_ with S_ % 4 == 0, so the
-        // previous chunk on a stage is this warp's own and its EMPTY parity waits are exact.
-        // GATHER: two plan entries per lane (keys lane, 32+lane; prefetched one owned chunk
-        // ahead), lanes 0-15 issue the tile::gather4s; K_ext bias rows are written before the
-        // K gathers (consumed by the S MMA, freed with KEMPTY), the keys for the causal mask
-        // before the V gathers (freed with VEMPTY).
-        static_assert(S_ % kLoadWarps == 0, "stage ownership");
-        const int g = (int)warp - kFirstLoadWarp;
-        int64_t c = 0;  // chunks of all previous items
+        // Warp (stage s = g >> 1, half h = g & 1) owns keys [64h, 64h+64) of every chunk on
+        // stage s: K_ext rows and K gathers after KEMPTY, then the keys for the causal mask and
+        // the V gathers after VEMPTY.  Whole half-chunks per warp keep the per-warp TMA issue
+        // (a fixed per-iteration cost plus ~70 clk per gather4) off the critical path
+        // (scripts/ubench_gather.cu); each warp waits only on its own stage's EMPTY phases.
+        const int g = loader_index(warp);
+        const int so = g >> 1, hh = g & 1;
+        const int kb = 64 * hh;  // first key of this warp's half
+        int64_t c = 0;           // chunks of all previous items
         for (int it = 0;; ++it) {
             const int slot = it & 1;
             mbar_wait(&bars[C::B_IFULL + slot], (it >> 1) & 1);
@@ -288,26 +324,26 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             if (I.n_chunks == 0) continue;
             const int64_t b = I.bh / p.Hq, h = I.bh % p.Hq;
             const int64_t bh_kv = b * p.Hkv + h / (p.Hq / p.Hkv);
-            int j = (int)(((int64_t)g - c % kLoadWarps + kLoadWarps) % kLoadWarps);  // first owned chunk
+            int j = (int)(((int64_t)so - c % S_ + S_) % S_);  // first chunk on stage `so`
             if constexpr (GATHER) {
                 const uint32_t* wlp = p.wl + I.base;
                 Chunk ch;
                 ch.len = 0;
                 ch.start = 0;
                 if (j < I.n_chunks) ch = chunk_info<true>(I, j);
-                uint32_t e0 = (int)lane < ch.len ? __ldg(wlp + ch.start + lane) : 0u;
-                uint32_t e1 = 32 + (int)lane < ch.len ? __ldg(wlp + ch.start + 32 + lane) : 0u;
-                for (; j < I.n_chunks; j += kLoadWarps) {
+                uint32_t e0 = kb + (int)lane < ch.len ? __ldg(wlp + ch.start + kb + lane) : 0u;
+                uint32_t e1 = kb + 32 + (int)lane < ch.len ? __ldg(wlp + ch.start + kb + 32 + lane) : 0u;
+                for (; j < I.n_chunks; j += S_) {
                     const int64_t cc = c + j;
                     const int s = (int)(cc % S_);
                     const int round = (int)(cc / S_);
                     Chunk chn;
                     chn.len = 0;
                     chn.start = 0;
-                    if (j + kLoadWarps < I.n_chunks) chn = chunk_info<true>(I, j + kLoadWarps);
-                    const uint32_t en0 = (int)lane < chn.len ? __ldg(wlp + chn.start + lane) : 0u;
-                    const uint32_t en1 = 32 + (int)lane < chn.len ? __ldg(wlp + chn.start + 32 + lane) : 0u;
-                    const bool ok0 = (int)lane < ch.len, ok1 = 32 + (int)lane < ch.len;
+                    if (j + S_ < I.n_chunks) chn = chunk_info<true>(I, j + S_);
+                    const uint32_t en0 = kb + (int)lane < chn.len ? __ldg(wlp + chn.start + kb + lane) : 0u;
+                    const uint32_t en1 = kb + 32 + (int)lane < chn.len ? __ldg(wlp + chn.start + kb + 32 + lane) : 0u;
+                    const bool ok0 = kb + (int)lane < ch.len, ok1 = kb + 32 + (int)lane < ch.len;
                     const uint32_t key0 = e0 & kKeyMask, key1 = e1 & kKeyMask;
                     const int r0 = (int)(bh_kv * p.N + (ok0 ? key0 : 0u));
                     const int r1 = (int)(bh_kv * p.N + (ok1 ? key1 : 0u));
@@ -320,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     const int ra = lo ? a0 : b0_, rb = lo ? a1 : b1_, rc = lo ? a2 : b2_, rd = lo ? a3 : b3_;
                     // ---- K: bias rows, then the gathers
                     if (lane == 0 && round > 0) mbar_wait(&bars[C::B_KEMPTY + s], (round - 1) & 1);
-                    if (lane == 0) trace(p, 0, cc);
+                    if (lane == 0 && hh == 0) trace(p, 0, cc);
                     __syncwarp();
                     {
                         // K_ext row: bias 0 for member blocks, -2^100 (bf16 0xF180) otherwise
@@ -331,14 +367,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                             const uint32_t x2 = (mem & 4u) ? 0u : 0xF180u, x3 = (mem & 8u) ? 0u : 0xF180u;
                             return make_uint4(x0 | (x1 << 16), x2 | (x3 << 16), 0u, 0u);
                         };
-                        *reinterpret_cast<uint4*>(kx + k16_offset((int)lane, 0)) = bias(m0);
-                        *reinterpret_cast<uint4*>(kx + k16_offset(32 + (int)lane, 0)) = bias(m1);
+                        *reinterpret_cast<uint4*>(kx + k16_offset(kb + (int)lane, 0)) = bias(m0);
+                        *reinterpret_cast<uint4*>(kx + k16_offset(kb + 32 + (int)lane, 0)) = bias(m1);
                         fence_proxy_async();  // generic-proxy smem write -> tcgen05.mma (async proxy)
                     }
                     __syncwarp();
-                    if (lane == 0) mbar_arrive_expect_tx(&bars[C::B_KFULL + s], kChunk * D * 2);
+                    if (lane == 0) mbar_arrive_expect_tx(&bars[C::B_KFULL + s], 64 * D * 2);
                     if (lane < 16) {
-                        uint8_t* dst = sK + s * C::kKVBytes + 4 * (int)lane * 128;
+                        uint8_t* dst = sK + s * C::kKVBytes + (kb + 4 * (int)lane) * 128;
 #pragma unroll
                         for (int cb = 0; cb < C::kCB; ++cb)
                             tma_gather4(dst + cb * kChunk * 128, &p.tm_k, &bars[C::B_KFULL + s], cb * 64, ra, rb, rc,
@@ -346,17 +382,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     }
                     // ---- V: keys for the causal mask, then the gathers
                     if (lane == 0 && round > 0) mbar_wait(&bars[C::B_VEMPTY + s], (round - 1) & 1);
-                    if (lane == 0) trace(p, 1, cc);
+                    if (lane == 0 && hh == 0) trace(p, 1, cc);
                     __syncwarp();
-                    sMeta[s * kChunk + lane] = ok0 ? key0 : kPad;
-                    sMeta[s * kChunk + 32 + lane] = ok1 ? key1 : kPad;
+                    sMeta[s * kChunk + kb + lane] = ok0 ? key0 : kPad;
+                    sMeta[s * kChunk + kb + 32 + lane] = ok1 ? key1 : kPad;
                     __syncwarp();
                     if (lane == 0) {
                         mbar_arrive(&bars[C::B_MFULL + s]);
-                        mbar_arrive_expect_tx(&bars[C::B_VFULL + s], kChunk * D * 2);
+                        mbar_arrive_expect_tx(&bars[C::B_VFULL + s], 64 * D * 2);
                     }
                     if (lane < 16) {
-                        uint8_t* dst = sV + s * C::kKVBytes + 4 * (int)lane * 128;
+                        uint8_t* dst = sV + s * C::kKVBytes + (kb + 4 * (int)lane) * 128;
 #pragma unroll
                         for (int cb = 0; cb < C::kCB; ++cb)
                             tma_gather4(dst + cb * kChunk * 128, &p.tm_v, &bars[C::B_VFULL + s], cb * 64, ra, rb, rc,
@@ -367,8 +403,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     ch = chn;
                 }
             } else {
-                if (lane == 0) {
-                    for (; j < I.n_chunks; j += kLoadWarps) {
+                if (lane == 0 && hh == 0) {
+                    for (; j < I.n_chunks; j += S_) {
                         const int64_t cc = c + j;
                         const int s = (int)(cc % S_);
                         const int round = (int)(cc / S_);
@@ -392,12 +428,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
         }
     } else if (warp == 1) {
         // ======================================== MMA issuer (single thread)
-        // Per chunk c: S_t(c+1) for the tiles of chunk c+1 (double-buffered S, so it can run
-        // ahead of the softmax of c), then PV_t(c) for the tiles of chunk c.
+        // Per item: S_t(first chunk of t) for both tiles; then for every chunk j in order and
+        // each tile t of j: PV_t(j) (after softmax_t(j)), then S_t(next chunk of t) -- issued
+        // after PV_t(j) because S_t overwrites P_t (in-order tensor pipe) and committed to
+        // SFULL_t, which therefore also certifies PV_t(j) complete.
         if (elect_one()) {
-            int64_t c = 0;                 // global chunk counter (stage rings)
-            uint32_t ns[2] = {0, 0};       // S issued per tile (buffer = ns & 1)
-            uint32_t np_[2] = {0, 0};      // PV issued per tile
+            int64_t c = 0;              // chunks of previous items (stage rings)
+            uint32_t np_[2] = {0, 0};   // PFULL_t phases consumed
             int qi = 0, oi = 0;
             const uint32_t qa = smem_u32(sQ);
             auto wait_k = [&](int64_t cc) {
@@ -405,12 +442,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                 tc_fence_after();
                 trace(p, 2, cc);
             };
-            auto issue_s = [&](int t, int64_t cc) {
+            auto issue_s = [&](int t, int64_t cc, int kmask) {
                 const int s = (int)(cc % S_);
-                const int bi = (int)(ns[t] & 1u);
                 const uint32_t ka = smem_u32(sK + s * C::kKVBytes);
                 const uint32_t q_t = qa + t * C::kQTileBytes;
-                const uint32_t st = tmem_base + s_col(t, bi);
+                const uint32_t st = tmem_base + s_col(t);
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                     const uint64_t adesc = make_sdesc(q_t + (kk >> 2) * 128 * 128 + (kk & 3) * 32, 16, 1024);
@@ -422,24 +458,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     const uint64_t bdesc = make_sdesc(smem_u32(smem + C::kOffKx + s * kChunk * 16 * 2), 128, 256, 0);
                     mma_bf16_ss(st, adesc, bdesc, C::kIdescS, 1u);
                 }
-                mma_commit(&bars[C::B_SFULL + 2 * t + bi]);
-                ++ns[t];
-            };
-            auto issue_pv = [&](int t, int64_t cc, bool first) {
-                const int s = (int)(cc % S_);
-                const int bi = (int)(np_[t] & 1u);
-                mbar_wait(&bars[C::B_PFULL + 2 * t + bi], (np_[t] >> 1) & 1u);
-                ++np_[t];
-                tc_fence_after();
-                const uint32_t pt = tmem_base + s_col(t, bi);
-                const uint32_t ot = tmem_base + 128u * t;
-                const uint32_t va = smem_u32(sV + s * C::kKVBytes);
-#pragma unroll
-                for (int kk = 0; kk < kChunk / 16; ++kk) {
-                    const uint64_t bdesc = make_sdesc(va + kk * 16 * 128, kChunk * 128, 1024);
-                    mma_bf16_ts(ot, pt + kk * 8, bdesc, C::kIdescPV, (first && kk == 0) ? 0u : 1u);
-                }
-                mma_commit(&bars[C::B_ODONE + t]);
+                mma_commit(&bars[C::B_SFULL + t]);
+                // K stage free once the last tile reading it has issued its S (tile 1 after tile 0)
+                if (t == (kmask == 1 ? 0 : 1)) mma_commit(&bars[C::B_KEMPTY + s]);
             };
             for (int it = 0;; ++it) {
                 const int slot = it & 1;
@@ -448,7 +469,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                 mbar_arrive(&bars[C::B_IEMPTY + slot]);
                 if (item < 0) break;
                 const Item I = decode_item<GATHER>(p, item);
-                if (I.n_chunks == 0) continue;
+                const int n = I.n_chunks;
+                if (n == 0) continue;
                 mbar_wait(&bars[C::B_QFULL], qi & 1);
                 ++qi;
                 if (oi > 0) {  // O_0 / O_1 of the previous item drained by the epilogues
@@ -456,56 +478,69 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     mbar_wait(&bars[C::B_OEMPTY + 1], (oi - 1) & 1);
                 }
                 ++oi;
+                tc_fence_after();
+                int nx[2];
+                nx[0] = (chunk_info<GATHER>(I, 0).mask & 1) ? 0 : next_chunk<GATHER>(I, 0, 0);
+                nx[1] = (chunk_info<GATHER>(I, 0).mask & 2) ? 0 : next_chunk<GATHER>(I, 1, 0);
                 bool started[2] = {false, false};
-                int m = chunk_info<GATHER>(I, 0).mask;
-                wait_k(c);
-                if (m & 1) issue_s(0, c);
-                if (m & 2) issue_s(1, c);
-                mma_commit(&bars[C::B_KEMPTY + (int)(c % S_)]);
-                if (I.n_chunks == 1) mma_commit(&bars[C::B_QEMPTY]);
-                for (int j = 0; j < I.n_chunks; ++j, ++c) {
-                    const int s = (int)(c % S_);
-                    const bool more = j + 1 < I.n_chunks;
-                    int mn = 0;
-                    if (more) {
-                        mn = chunk_info<GATHER>(I, j + 1).mask;
-                        wait_k(c + 1);
-                        if (mn & 1) issue_s(0, c + 1);
-                        if (mn & 2) issue_s(1, c + 1);
-                        mma_commit(&bars[C::B_KEMPTY + (int)((c + 1) % S_)]);
-                        if (j + 2 == I.n_chunks) mma_commit(&bars[C::B_QEMPTY]);
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    if (nx[t] < n) {
+                        wait_k(c + nx[t]);
+                        issue_s(t, c + nx[t], chunk_info<GATHER>(I, nx[t]).mask);
                     }
-                    mbar_wait(&bars[C::B_VFULL + s], (uint32_t)((c / S_) & 1));
-                    trace(p, 3, c);
+                }
+                for (int j = 0; j < n; ++j) {
+                    const int64_t cc = c + j;
+                    const int s = (int)(cc % S_);
+                    const int m = chunk_info<GATHER>(I, j).mask;
+                    mbar_wait(&bars[C::B_VFULL + s], (uint32_t)((cc / S_) & 1));
+                    trace(p, 3, cc);
 #pragma unroll
                     for (int t = 0; t < 2; ++t) {
                         if (!(m & (1 << t))) continue;
-                        issue_pv(t, c, !started[t]);
+                        mbar_wait(&bars[C::B_PFULL + t], np_[t] & 1u);
+                        ++np_[t];
+                        tc_fence_after();
+                        const uint32_t pt = tmem_base + s_col(t);
+                        const uint32_t ot = tmem_base + o_col(t);
+                        const uint32_t va = smem_u32(sV + s * C::kKVBytes);
+#pragma unroll
+                        for (int kk = 0; kk < kChunk / 16; ++kk) {
+                            const uint64_t bdesc = make_sdesc(va + kk * 16 * 128, kChunk * 128, 1024);
+                            mma_bf16_ts(ot, pt + kk * 8, bdesc, C::kIdescPV, (!started[t] && kk == 0) ? 0u : 1u);
+                        }
                         started[t] = true;
-                        trace(p, 4 + t, c);
+                        trace(p, 4 + t, cc);
+                        const int x = next_chunk<GATHER>(I, t, j);
+                        if (x < n) {
+                            wait_k(c + x);
+                            issue_s(t, c + x, chunk_info<GATHER>(I, x).mask);
+                        }
                     }
                     mma_commit(&bars[C::B_VEMPTY + s]);
-                    m = mn;
                 }
-                // O_0 / O_1 final for this item (one phase per item with chunks, both tiles)
-                mma_commit(&bars[C::B_OFIN + 0]);
-                mma_commit(&bars[C::B_OFIN + 1]);
+                mma_commit(&bars[C::B_QEMPTY]);  // Q tiles free (every S of the item issued)
+                mma_commit(&bars[C::B_OFIN]);    // every MMA of the item complete
+                c += n;
             }
         }
         __syncwarp();
+    }
     } else {
+        setmaxnreg_inc192();
         // ======================================== softmax / epilogue (two warpgroups)
-        const int tile = ((int)warp - 2) >> 2;
+        const int tile = ((int)warp - 4) >> 2;
         const uint32_t quad = warp & 3u;
         const int r = (int)(quad * 32 + lane);
         const uint32_t lane_off = (quad * 32u) << 16;
-        const uint32_t tO = tmem_base + lane_off + 128u * tile;
+        const uint32_t tO = tmem_base + lane_off + o_col(tile);
+        const uint32_t tS = tmem_base + lane_off + s_col(tile);
         const int row_in_item = 128 * tile + r;
         const float sl2 = p.scale_log2;
         int64_t c = 0;
-        uint32_t ct = 0;  // this tile's chunk counter (S buffer = ct & 1)
-        uint32_t od = 0;  // ODONE phases known complete (= PVs of this tile known finished)
-        uint32_t fi = 0;  // OFIN phases waited (items with chunks)
+        uint32_t ns = 0;  // SFULL_t phases consumed
+        uint32_t fi = 0;  // OFIN phases consumed (items with chunks)
         for (int it = 0;; ++it) {
             const int slot = it & 1;
             mbar_wait(&bars[C::B_IFULL + slot], (it >> 1) & 1);
@@ -515,70 +550,73 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             const Item I = decode_item<GATHER>(p, item);
             const int64_t qrow = I.it * 256 + row_in_item;
             const bool row_ok = qrow < p.N;
+            const int64_t qrow_w0 = I.it * 256 + 128 * tile + 32 * quad;  // warp's first row
             float m_ref = -INFINITY;  // log2-domain reference max (lazy rescaling)
             float2 lsum2 = make_float2(0.f, 0.f);
             int jt = 0;  // chunks of this item processed by this tile
             for (int j = 0; j < I.n_chunks; ++j, ++c) {
                 const int s = (int)(c % S_);
-                if (!(chunk_info<GATHER>(I, j).mask & (1 << tile))) continue;
-                const int bi = (int)(ct & 1u);
-                const uint32_t tS = tmem_base + lane_off + s_col(tile, bi);
-                uint32_t mw[2];
+                const Chunk chk = chunk_info<GATHER>(I, j);
+                if (!(chk.mask & (1 << tile))) continue;
+                // ---- causal / ragged prefix (per row): visible columns [0, lo)
+                bool need_prefix = false;
+                int lo = kChunk;
                 if constexpr (GATHER) {
-                    mw[0] = mw[1] = 0xffffffffu;  // membership is applied by the MMA
                     if (p.causal) {
                         mbar_wait(&bars[C::B_MFULL + s], (uint32_t)((c / S_) & 1));
                         const uint32_t* meta = sMeta + s * kChunk;
-                        int lo = 0, hi = kChunk;  // keys ascending: visible = prefix with key <= qrow
-                        while (lo < hi) {
-                            const int mid = (lo + hi) >> 1;
-                            if ((int64_t)meta[mid] <= qrow) lo = mid + 1;
-                            else hi = mid;
+                        if ((int64_t)meta[kChunk - 1] > qrow_w0) {  // (padding sorts last)
+                            need_prefix = true;
+                            int a_ = 0, b_ = kChunk;  // keys ascending: visible = prefix with key <= qrow
+                            while (a_ < b_) {
+                                const int mid = (a_ + b_) >> 1;
+                                if ((int64_t)meta[mid] <= qrow) a_ = mid + 1;
+                                else b_ = mid;
+                            }
+                            lo = a_;
                         }
-                        mw[0] = prefix_mask(lo);
-                        mw[1] = prefix_mask(lo - 32);
                     }
                 } else {
-                    const int64_t vend = p.causal ? min(p.N, qrow + 1) : p.N;
-                    const int64_t nv = vend - (int64_t)j * kChunk;
-                    mw[0] = prefix_mask(nv);
-                    mw[1] = prefix_mask(nv - 32);
-                }
-                const bool full = (mw[0] & mw[1]) == 0xffffffffu;
-                mbar_wait(&bars[C::B_SFULL + 2 * tile + bi], (ct >> 1) & 1u);
-                tc_fence_after();
-                if (lane == 0 && (warp == 2 || warp == 6)) trace(p, 6 + 2 * tile, c);
-                __syncwarp();  // reconverge after the per-row causal search (tcgen05.ld is .sync.aligned)
-                // ---- single TMEM pass (TMEM reads, 64 B/clk/SM, bind at D = 128): S -> registers,
-                // masked row max, lazy O rescale, P = exp2(s*scale*log2e - m) bf16-packed over S.
-                uint32_t a[32], b[32];
-                tmem_ld32(tS, a);
-                tmem_ld32(tS + 32, b);
-                tmem_ld_wait();
-                if (!full) {  // causal / ragged tail only: masked scores -> -inf (exp2 -> 0)
-#pragma unroll
-                    for (int t = 0; t < 32; ++t) {
-                        a[t] = (mw[0] & (1u << t)) ? a[t] : 0xff800000u;
-                        b[t] = (mw[1] & (1u << t)) ? b[t] : 0xff800000u;
+                    const int64_t k0 = (int64_t)j * kChunk;
+                    if (chk.len < kChunk || (p.causal && k0 + kChunk - 1 > qrow_w0)) {
+                        need_prefix = true;
+                        const int64_t vend = p.causal ? min((int64_t)chk.len, qrow - k0 + 1) : (int64_t)chk.len;
+                        lo = (int)max((int64_t)0, min((int64_t)kChunk, vend));
                     }
                 }
+                need_prefix = __any_sync(0xffffffffu, need_prefix);  // warp-uniform branch below
+                mbar_wait(&bars[C::B_SFULL + tile], ns & 1u);
+                ++ns;
+                tc_fence_after();
+                if (lane == 0 && (warp == 4 || warp == 8)) trace(p, 6 + 2 * tile, c);
+                __syncwarp();
+                // ---- one TMEM pass: the row's 128 S columns -> registers (192-register budget),
+                // masked row max, lazy O rescale, P = exp2(s*scale*log2e - m) bf16-packed over
+                // S_t's first 64 columns (every S column is already in registers)
+                uint32_t a[128];
+#pragma unroll
+                for (int qd = 0; qd < 4; ++qd) {
+                    uint32_t (&aq)[32] = *reinterpret_cast<uint32_t(*)[32]>(a + 32 * qd);
+                    tmem_ld32(tS + 32 * qd, aq);
+                }
+                tmem_ld_wait();
+                if (need_prefix) {
+#pragma unroll
+                    for (int t = 0; t < 128; ++t) a[t] = (t < lo) ? a[t] : kNegInfBits;
+                }
                 float mx;
-                {  // 4 independent FMNMX3 chains (latency), then combine
+                {
                     float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                    for (int t = 0; t < 32; t += 4) {
+                    for (int t = 0; t < 128; t += 8) {
                         m4[0] = fmaxf(fmaxf(m4[0], __uint_as_float(a[t])), __uint_as_float(a[t + 1]));
                         m4[1] = fmaxf(fmaxf(m4[1], __uint_as_float(a[t + 2])), __uint_as_float(a[t + 3]));
-                        m4[2] = fmaxf(fmaxf(m4[2], __uint_as_float(b[t])), __uint_as_float(b[t + 1]));
-                        m4[3] = fmaxf(fmaxf(m4[3], __uint_as_float(b[t + 2])), __uint_as_float(b[t + 3]));
+                        m4[2] = fmaxf(fmaxf(m4[2], __uint_as_float(a[t + 4])), __uint_as_float(a[t + 5]));
+                        m4[3] = fmaxf(fmaxf(m4[3], __uint_as_float(a[t + 6])), __uint_as_float(a[t + 7]));
                     }
                     mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
                 }
                 const float m_new = fmaxf(m_ref, mx * sl2);
-                // SFULL(ct) fired, so every MMA issued before S(ct) -- including PV(ct-2) of
-                // this tile -- is complete: ODONE phases 0..ct-2 are done (parity waits on
-                // phase ct-1 are then unambiguous).
-                if (ct >= 1 && od < ct - 1) od = ct - 1;
                 const bool need = m_new > m_ref + 8.0f;
                 const float corr = need ? ex2(m_ref - m_new) : 1.0f;
                 if (need) {
@@ -586,19 +624,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     lsum2.y *= corr;
                     m_ref = m_new;
                 }
+                // SFULL_t(c) certifies PV_t of this tile's previous chunk complete: O_t is stable.
                 if (jt > 0 && __any_sync(0xffffffffu, need)) {
-                    // O_t must be stable (PV_t of this tile's previous chunk done) before the
-                    // rescale; without a rescale the softmax never waits on the PV pipeline.
-                    for (; od < ct; ++od) mbar_wait(&bars[C::B_ODONE + tile], od & 1u);
-                    tc_fence_after();
 #pragma unroll
-                    for (int g = 0; g < D / 8; ++g) {
+                    for (int gq = 0; gq < D / 8; ++gq) {
                         uint32_t o[8];
-                        tmem_ld8(tO + g * 8, o);
+                        tmem_ld8(tO + gq * 8, o);
                         tmem_ld_wait();
 #pragma unroll
                         for (int t = 0; t < 8; ++t) o[t] = __float_as_uint(__uint_as_float(o[t]) * corr);
-                        tmem_st8(tO + g * 8, o);
+                        tmem_st8(tO + gq * 8, o);
                     }
                     tmem_st_wait();
                 }
@@ -606,53 +641,62 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
                     const uint64_t sl2x2 = pack_f32x2(sl2, sl2);
                     const uint64_t nmx2 = pack_f32x2(neg_m, neg_m);
-                    uint32_t pk[32];
 #pragma unroll
-                    for (int t = 0; t < 32; t += 2) {
-                        const float2 xa = unpack_f32x2(
-                            ffma2(pack_f32x2(__uint_as_float(a[t]), __uint_as_float(a[t + 1])), sl2x2, nmx2));
-                        const float2 xb = unpack_f32x2(
-                            ffma2(pack_f32x2(__uint_as_float(b[t]), __uint_as_float(b[t + 1])), sl2x2, nmx2));
-                        const float p0 = ex2(xa.x), p1 = ex2(xa.y), p2 = ex2(xb.x), p3 = ex2(xb.y);
-                        lsum2 = fadd2(lsum2, fadd2(make_float2(p0, p1), make_float2(p2, p3)));
-                        pk[t >> 1] = pack_bf16x2(p0, p1);
-                        pk[16 + (t >> 1)] = pack_bf16x2(p2, p3);
+                    for (int qd = 0; qd < 4; ++qd) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int t0 = 0; t0 < 32; t0 += 4) {
+                            const int t = 32 * qd + t0;
+                            const float2 xa = unpack_f32x2(
+                                ffma2(pack_f32x2(__uint_as_float(a[t]), __uint_as_float(a[t + 1])), sl2x2, nmx2));
+                            const float2 xb = unpack_f32x2(
+                                ffma2(pack_f32x2(__uint_as_float(a[t + 2]), __uint_as_float(a[t + 3])), sl2x2, nmx2));
+                            float p0, p1, p2, p3;
+                            if ((t >> 2) % kPolyEvery == kPolyEvery - 1) {  // FMA-pipe exp2 (MUFU offload)
+                                const float2 pa = ex2_poly2(xa.x, xa.y), pb = ex2_poly2(xb.x, xb.y);
+                                p0 = pa.x, p1 = pa.y, p2 = pb.x, p3 = pb.y;
+                            } else {
+                                p0 = ex2(xa.x), p1 = ex2(xa.y), p2 = ex2(xb.x), p3 = ex2(xb.y);
+                            }
+                            lsum2 = fadd2(lsum2, fadd2(make_float2(p0, p1), make_float2(p2, p3)));
+                            pk[t0 >> 1] = pack_bf16x2(p0, p1);
+                            pk[(t0 >> 1) + 1] = pack_bf16x2(p2, p3);
+                        }
+                        tmem_st16(tS + 16 * qd, pk);
                     }
-                    tmem_st32(tS, pk);
                     tmem_st_wait();
                 }
                 tc_fence_before();
-                mbar_arrive(&bars[C::B_PFULL + 2 * tile + bi]);
-                if (lane == 0 && (warp == 2 || warp == 6)) trace(p, 7 + 2 * tile, c);
-                ++ct;
+                mbar_arrive(&bars[C::B_PFULL + tile]);
+                if (lane == 0 && (warp == 4 || warp == 8)) trace(p, 7 + 2 * tile, c);
                 ++jt;
             }
             // ---------------------------------------------------------------- epilogue
-            // rows that only ever saw masked keys carry m_ref ~ -2^100*scale*log2e: no visible key
+            // rows that only ever saw masked keys: l = 0 (non-members -> -2^100 -> 0), degenerate
             const float l = (m_ref < -1e28f) ? 0.f : lsum2.x + lsum2.y;
             const float inv = l > 0.f ? 1.f / l : 0.f;
             __nv_bfloat16* orow = p.o + (I.bh * p.N + qrow) * D;
-            if (I.n_chunks > 0) {  // every PV of the item complete (ODONE parity may be 2 behind here)
-                mbar_wait(&bars[C::B_OFIN + tile], fi & 1u);
+            if (I.n_chunks > 0) {  // every MMA of the item complete (one OFIN phase per item with chunks)
+                mbar_wait(&bars[C::B_OFIN], fi & 1u);
                 ++fi;
+                tc_fence_after();
             }
             if (jt > 0) {
                 __syncwarp();
-                tc_fence_after();
 #pragma unroll
-                for (int g = 0; g < D / 32; ++g) {
+                for (int gq = 0; gq < D / 32; ++gq) {
                     uint32_t ov[32];
-                    tmem_ld32(tO + g * 32, ov);
+                    tmem_ld32(tO + gq * 32, ov);
                     tmem_ld_wait();
                     if (row_ok && l > 0.f) {
 #pragma unroll
                         for (int t = 0; t < 32; t += 8) {
-                            uint4 w;
-                            w.x = pack_bf16x2(__uint_as_float(ov[t]) * inv, __uint_as_float(ov[t + 1]) * inv);
-                            w.y = pack_bf16x2(__uint_as_float(ov[t + 2]) * inv, __uint_as_float(ov[t + 3]) * inv);
-                            w.z = pack_bf16x2(__uint_as_float(ov[t + 4]) * inv, __uint_as_float(ov[t + 5]) * inv);
-                            w.w = pack_bf16x2(__uint_as_float(ov[t + 6]) * inv, __uint_as_float(ov[t + 7]) * inv);
-                            *reinterpret_cast<uint4*>(orow + g * 32 + t) = w;
+                            uint4 w4;
+                            w4.x = pack_bf16x2(__uint_as_float(ov[t]) * inv, __uint_as_float(ov[t + 1]) * inv);
+                            w4.y = pack_bf16x2(__uint_as_float(ov[t + 2]) * inv, __uint_as_float(ov[t + 3]) * inv);
+                            w4.z = pack_bf16x2(__uint_as_float(ov[t + 4]) * inv, __uint_as_float(ov[t + 5]) * inv);
+                            w4.w = pack_bf16x2(__uint_as_float(ov[t + 6]) * inv, __uint_as_float(ov[t + 7]) * inv);
+                            *reinterpret_cast<uint4*>(orow + gq * 32 + t) = w4;
                         }
                     }
                 }
@@ -888,6 +932,10 @@ static cudaError_t launch_attn_t(const AttnParams& p, int grid, cudaStream_t st)
 }
 
 cudaError_t launch_attn(const AttnParams& p, int D, bool gather, int grid, cudaStream_t st) {
+    // Non-causal sparse plans are dominated by chunks of one tile (segments tile 0 / tile 1
+    // only), where the double-buffered 64-key kernel (attn_db.cu) is faster; the 128-key
+    // ping-pong kernel wins for dense and causal (profiles/sweep_r01.md vs sweep_r01v6.md).
+    if (gather && !p.causal) return launch_attn_db(p, D, grid, st);
     if (D == 128) return gather ? launch_attn_t<128, true>(p, grid, st) : launch_attn_t<128, false>(p, grid, st);
     if (D == 64) return gather ? launch_attn_t<64, true>(p, grid, st) : launch_attn_t<64, false>(p, grid, st);
     return cudaErrorInvalidValue;

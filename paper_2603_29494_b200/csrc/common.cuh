@@ -147,6 +147,14 @@ VA_DEV void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
                  "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                  : "memory");
 }
+VA_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
 VA_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 VA_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
@@ -226,10 +234,10 @@ VA_DEV float2 fadd2(float2 a, float2 b) {
 // exp2 on the FMA pipe for two lanes (FA4-style MUFU offload): round-to-nearest split
 // x = i + f (f in [-0.5, 0.5]) via the 1.5*2^23 magic add, 2^f by a degree-3 minimax
 // polynomial (max relative error 1.0e-4, well below bf16's 2^-9), 2^i by an integer add
-// to the exponent field.  Inputs clamped at -125 (results below 2^-125 are ~0 anyway).
-VA_DEV float2 ex2_poly2(float x0, float x1) {
-    x0 = fmaxf(x0, -125.f);
-    x1 = fmaxf(x1, -125.f);
+// to the exponent field.  Inputs below -125 give exactly 0.
+VA_DEV float2 ex2_poly2(float x0_in, float x1_in) {
+    const float x0 = fmaxf(x0_in, -125.f);
+    const float x1 = fmaxf(x1_in, -125.f);
     const uint64_t X = pack_f32x2(x0, x1);
     const uint64_t T = ffma2(X, pack_f32x2(1.f, 1.f), pack_f32x2(12582912.f, 12582912.f));
     const uint64_t R = ffma2(T, pack_f32x2(1.f, 1.f), pack_f32x2(-12582912.f, -12582912.f));
@@ -239,8 +247,9 @@ VA_DEV float2 ex2_poly2(float x0, float x1) {
     P = ffma2(P, F, pack_f32x2(0.693286120891571f, 0.693286120891571f));
     P = ffma2(P, F, pack_f32x2(1.f, 1.f));
     const float2 p = unpack_f32x2(P), t = unpack_f32x2(T);
-    return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
-                       __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+    // exact 0 below the clamp (masked scores are -inf / -2^100; like ex2.approx.ftz, which flushes)
+    return make_float2(x0_in < -125.f ? 0.f : __uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                       x1_in < -125.f ? 0.f : __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
 }
 // Order-preserving map fp32 -> u32 (a < b  <=>  key(a) < key(b) for non-NaN).
 VA_DEV uint32_t f32_order_key(float f) {

@@ -582,8 +582,8 @@ vecattn_status_t vecattn_dense_fwd(const vecattn_problem_t* p, const void* q, co
     AttnParams* ap = new AttnParams;
     st = attn_common(p, q, k, v, o, lse, *ap);
     if (st == VECATTN_OK &&
-        (!tmap_3d(&ap->tm_k, k, (uint64_t)p->D, (uint64_t)p->N, (uint64_t)(p->B * p->Hkv), 64) ||
-         !tmap_3d(&ap->tm_v, v, (uint64_t)p->D, (uint64_t)p->N, (uint64_t)(p->B * p->Hkv), 64)))
+        (!tmap_3d(&ap->tm_k, k, (uint64_t)p->D, (uint64_t)p->N, (uint64_t)(p->B * p->Hkv), 128) ||
+         !tmap_3d(&ap->tm_v, v, (uint64_t)p->D, (uint64_t)p->N, (uint64_t)(p->B * p->Hkv), 128)))
         st = VECATTN_ERR_UNSUPPORTED;
     if (st != VECATTN_OK) { delete ap; return st; }
     ap->Np = (p->N + 127) / 128;
