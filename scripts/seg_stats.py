@@ -24,9 +24,13 @@ n_it = (wl.N + 255) // 256
 lens = ws[base: base + H * n_it * 12].view(torch.int32).view(-1, 3).cpu().numpy().astype(np.int64)
 lb, l0, l1 = lens[:, 0], lens[:, 1], lens[:, 2]
 ch = lambda x: (x + 127) // 128
+ch64 = lambda x: (x + 63) // 64
 nnz = int(off[-1])
 pairs = lb + l0, lb + l1
 print(f"nnz={nnz} sum(lb)={lb.sum()} sum(l0)={l0.sum()} sum(l1)={l1.sum()}  both-fraction={lb.sum()/(lb+l0+l1).sum():.3f}")
 print(f"gathered keys: seg={ (lb+l0+l1).sum() }  pair-design={ (2*lb+l0+l1).sum() }  per-block sum={nnz}")
 print(f"tile-chunks executed: seg={(2*ch(lb)+ch(l0)+ch(l1)).sum()}  pair-design={(ch(lb+l0)+ch(lb+l1)).sum()}  quad-union={(2*ch(lb+l0+l1)).sum()}")
 print(f"chunks gathered: seg={(ch(lb)+ch(l0)+ch(l1)).sum()} pair={(ch(lb+l0)+ch(lb+l1)).sum()}")
+m = np.minimum(ch(l0), ch(l1))
+tail = np.abs(ch(l0) - ch(l1))
+print(f"128-key chunks: shared={ch(lb).sum()} interleaved-pairs={2*m.sum()} single-tile tail={tail.sum()}")
