@@ -500,7 +500,8 @@ def run_ours(args):
                             "frac": round(float(sel_bytes_all[0]) / ws / (sel_stage_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
                             "algorithmic_bytes": int(sel_bytes_all[0] / ws),
                             "note": "pool + selection GEMM/filter + scan; SURVEY 8(d): tensor/issue-bound at rho >= 0.75"},
-        "roofline": {"bound": "tensor", "kernel": "attn_kernel<128,gather> (attention kernel alone, vecattn_forward)",
+        "roofline": {"bound": "tensor", "kernel": ("attn_kernel<128,gather>" if causal else "attn_db_kernel<128,gather>") +
+                     " (attention kernel alone, vecattn_forward)",
                      "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "traffic_note": "dram read+write bytes per launch from profiles/traffic.json (ncu --set full)",

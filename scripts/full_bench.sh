@@ -10,7 +10,7 @@ timeout 1200 /usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum --clock-co
   --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --alpha 1.0039 --dense-reps 1 \
   > gpurun_out/launches_$TAG.log 2>&1
 # full-size sparse kernel (fused forward, 24 heads): 1 select pass then the attention launch
-timeout 1200 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:attn_kernel -s 0 -c 1 \
+timeout 1200 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:attn_db_kernel -s 0 -c 1 \
   -o gpurun_out/prof_$TAG -f python scripts/prof_run.py --reps 1 --no-dense --fused > gpurun_out/prof_$TAG.log 2>&1
 python scripts/summarize_ncu.py $TAG > /dev/null 2>&1
 fi

@@ -18,7 +18,7 @@ if os.path.exists(lf):
     for r in rows[hi + 1:]:
         if len(r) > vi and r[mi] == "gpu__time_duration.sum":
             agg.setdefault(r[ki], []).append(float(r[vi].replace(",", "")) / 1e6)
-    ours = {k: v for k, v in agg.items() if "va::" in k or "attn_kernel" in k or "select_kernel" in k}
+    ours = {k: v for k, v in agg.items() if "va::" in k or "attn_" in k or "select_kernel" in k}
     lines += ["## Launch list (gpu__time_duration.sum, --clock-control none; cold-cache, serialised)", "",
               "Source command: `ncu --metrics gpu__time_duration.sum --clock-control none --csv "
               "python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --alpha 1.0039 --dense-reps 1`", "",
@@ -31,7 +31,8 @@ if os.path.exists(lf):
         return sum(xs) / len(xs) if xs else 0.0
     # one vecattn_forward step (the bench's timed call): pool, select, scan, emit (CSR), plan, attention
     step = {n: mean(n) for n in ["pool_kernel", "select_kernel", "scan_kernel", "emit_kernel", "plan_kernel"]}
-    sp = [x for k, v in ours.items() if "attn_kernel<128, 1>" in k or "attn_kernel<128, true>" in k for x in v]
+    sp = [x for k, v in ours.items() if "attn_db_kernel<128" in k or "attn_kernel<128, 1>" in k or "attn_kernel<128, true>" in k
+          for x in v]
     step["attn_kernel<gather>"] = sum(sp) / len(sp) if sp else 0.0
     tot = sum(step.values())
     lines += ["", "Per-step shares (one vecattn_forward call = the bench step):", "", "| stage | ms | share |", "|---|---|---|"]
@@ -67,7 +68,7 @@ if os.path.exists(rep):
 open(os.path.join(out_dir, f"ncu_{tag}.md"), "w").write("\n".join(lines) + "\n")
 # per-launch DRAM traffic of the sparse attention kernel (bench.py roofline.traffic)
 for name, d in summary.items():
-    if "attn_kernel<128, 1>" in name or "attn_kernel<128, true>" in name:
+    if "attn_db_kernel<128" in name or "attn_kernel<128, 1>" in name or "attn_kernel<128, true>" in name:
         def num(x):
             v, u = x.split()[0], x.split()[1] if len(x.split()) > 1 else ""
             mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(u, 1)
