@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--mode", default="alg1", choices=["alg1", "exact", "topk"])
     ap.add_argument("--rho", type=float, default=0.785)
     ap.add_argument("--alpha", type=float, default=None, help="skip calibration")
+    ap.add_argument("--pq", type=int, default=64, help="query-block (vector) size P_q (64 or 128)")
+    ap.add_argument("--bk", type=int, default=16, help="Alg. 1 semantic K-tile size B_K")
+    ap.add_argument("--gk", type=int, default=0, help="Alg. 1 tiles per group G_K (0 = the workload's)")
     ap.add_argument("--dense-reps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -237,7 +240,7 @@ def run_ours(args):
 
     wl = synth.WORKLOADS[args.workload]
     B, H, Hkv, N, D, causal = wl.B, wl.Hq, wl.Hkv, wl.N, wl.D, wl.causal
-    pq, bk, gk = 64, 16, wl.gk
+    pq, bk, gk = args.pq, args.bk, (args.gk or wl.gk)
     h0, h1, hmax = head_range(H, ws, rank)
     Hl = h1 - h0
 

@@ -8,15 +8,16 @@ out = [f"# Sweep {tag} (1xB200, kernel-only bench lines; `scripts/sweep.sh`)", "
        "alpha calibrated by bisection to the target sparsity (MINS_ALG1 unless noted). `fwd` = one vecattn_forward",
        "(pool, select, scan, CSR emit, plan, attention); speed-up = dense / fwd; attention TFLOP/s = useful",
        "4*D*sum|J_r| flops / attention-kernel time; select GB/s = algorithmic bytes / (pool+select+scan) time.", "",
-       "| workload | kind | mode | causal | H/Hkv | N | rho | fwd ms | select ms | plan ms | attn ms | dense ms | speed-up | attn TFLOP/s (frac) | dense TFLOP/s | select GB/s | SM MHz |",
-       "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+       "| workload | kind | mode | causal | H/Hkv | N | P_q | B_K | G_K | rho | fwd ms | select ms | plan ms | attn ms | dense ms | speed-up | attn TFLOP/s (frac) | dense TFLOP/s | select GB/s | SM MHz |",
+       "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
 for d in rows:
     c = d["config"]; st = d.get("stage_ms", {}); sr = d.get("select_roofline", {})
     kind = "gauss" if "GAUSS" in d.get("data", "") else "video"
     out.append(f"| {c['workload']} | {kind} | {c['mode']} | {c['causal']} | {c['H']}/{c['Hkv']} | {c['N']} | "
+               f"{c['pq']} | {c['bk']} | {c['gk']} | "
                f"{c['rho_achieved']:.3f} | {d['forward_ms']:.2f} | {st.get('select', -1):.2f} | {st.get('emit_plan', -1):.2f} | "
-               f"{st.get('attention', -1):.2f} | {d['dense_ms']:.1f} | {d['speedup_vs_dense']:.2f} | "
-               f"{d['roofline']['achieved']:.0f} ({d['roofline']['frac']:.2f}) | {d['dense_tflops']:.0f} | "
+               f"{st.get('attention', -1):.2f} | {(d['dense_ms'] or float('nan')):.1f} | {(d['speedup_vs_dense'] or float('nan')):.2f} | "
+               f"{d['roofline']['achieved']:.0f} ({d['roofline']['frac']:.2f}) | {(d['dense_tflops'] or float('nan')):.0f} | "
                f"{sr.get('achieved', 0):.0f} | {d['clocks']['sm_mhz']:.0f} |")
 open(os.path.join(ROOT, "profiles", f"sweep_{tag}.md"), "w").write("\n".join(out) + "\n")
 print("\n".join(out))
