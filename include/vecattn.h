@@ -145,6 +145,24 @@ VECATTN_API size_t vecattn_dense_workspace_bytes(const vecattn_problem_t* p);
 VECATTN_API vecattn_status_t vecattn_dense_fwd(const vecattn_problem_t* p, const void* q, const void* k, const void* v,
                                    void* o, float* lse, void* ws, size_t ws_bytes, vecattn_stream_t stream);
 
+/* ------------------------------------------------ per-head filter ratios (Eq. 4) */
+
+/* Dynamic programming for the offline search of per-head filter ratios, Eq. 4.
+ * Host-only: no GPU work, callable without a device.  sp and perf are row-major HOST arrays
+ * [H][n_cand]: the sparsity sp_h(alpha_c) in [0, 1] and the performance Perf_h(alpha_c) of
+ * head h under candidate filter ratio c, recorded offline by sampling.
+ * DP[h][rho] of Eq. 4 -- the best total performance of the first h heads at average
+ * sparsity rho -- is run on the running sparsity sum h*rho, quantised to 1/grid (round half
+ * up), with the target read as a floor: the result maximises sum_h Perf_h(alpha_h) subject
+ * to (1/H) sum_h sp_h(alpha_h) >= rho_target (reading R17b).  Among optimal
+ * assignments the lexicographically smallest candidate sequence is returned.
+ * Writes choice[H] (candidate index per head) and *best (the optimal total performance).
+ * Errors: VECATTN_ERR_INVALID_ARGUMENT for NULL pointers, H < 1, n_cand < 1, grid < 1,
+ * rho_target outside [0, 1], non-finite or out-of-range inputs, or when no assignment
+ * reaches the target (then *best = -inf and choice is untouched).  O(H * n_cand * H * grid). */
+VECATTN_API vecattn_status_t vecattn_alpha_dp(int32_t H, int32_t n_cand, const float* sp, const float* perf,
+                                              float rho_target, int32_t grid, int32_t* choice, double* best);
+
 /* ------------------------------------------------ naive selection baselines */
 
 /* The paper's NAIVE materialise-then-filter selection (Fig. 5), the

@@ -8,6 +8,9 @@
 #include <cudaTypedefs.h>
 #include <math.h>
 #include <mutex>
+#include <vector>
+#include <limits>
+#include <cmath>
 #include <stdlib.h>
 #include <string.h>
 
@@ -290,6 +293,54 @@ vecattn_status_t vecattn_kernel_timing_last(float* select_ms, float* plan_ms, fl
     if (g_timing.has_sel) cudaEventElapsedTime(select_ms, g_timing.ev[0], g_timing.ev[1]);
     if (g_timing.has_plan) cudaEventElapsedTime(plan_ms, g_timing.ev[1], g_timing.ev[2]);
     if (g_timing.has_attn) cudaEventElapsedTime(attn_ms, g_timing.ev[2], g_timing.ev[3]);
+    return VECATTN_OK;
+}
+
+// ------------------------------------------------------------ per-head filter ratios (Eq. 4)
+// Eq. 4 run backwards over heads on the quantised sparsity sum s (capped at the
+// target, since any sum >= target is equivalent): F[h][s] = best performance of heads
+// h..H-1 given the sum s of heads 0..h-1; F[H][s] = 0 if s >= need else -inf.  The forward
+// reconstruction takes the smallest candidate attaining F at every head.
+vecattn_status_t vecattn_alpha_dp(int32_t H, int32_t n_cand, const float* sp, const float* perf, float rho_target,
+                                  int32_t grid, int32_t* choice, double* best) {
+    if (!sp || !perf || !choice || !best || H < 1 || n_cand < 1 || grid < 1 || !(rho_target >= 0.f) ||
+        !(rho_target <= 1.f))
+        return VECATTN_ERR_INVALID_ARGUMENT;
+    const int64_t C = n_cand;
+    std::vector<int64_t> q((size_t)H * C);
+    for (int64_t x = 0; x < (int64_t)H * C; ++x) {
+        if (!std::isfinite(sp[x]) || !std::isfinite(perf[x]) || sp[x] < 0.f || sp[x] > 1.f)
+            return VECATTN_ERR_INVALID_ARGUMENT;
+        q[x] = (int64_t)std::floor((double)sp[x] * grid + 0.5);
+    }
+    const int64_t need = (int64_t)std::floor((double)rho_target * grid * H + 0.5);
+    const double NEG = -std::numeric_limits<double>::infinity();
+    std::vector<double> F((size_t)(H + 1) * (need + 1), NEG);
+    auto at = [&](int64_t h, int64_t s) -> double& { return F[(size_t)h * (need + 1) + s]; };
+    at(H, need) = 0.0;
+    for (int64_t h = H - 1; h >= 0; --h)
+        for (int64_t s = 0; s <= need; ++s) {
+            double bestv = NEG;
+            for (int64_t c = 0; c < C; ++c) {
+                const double nxt = at(h + 1, std::min(need, s + q[h * C + c]));
+                if (nxt == NEG) continue;
+                bestv = std::max(bestv, (double)perf[h * C + c] + nxt);
+            }
+            at(h, s) = bestv;
+        }
+    *best = at(0, 0);
+    if (*best == NEG) return VECATTN_ERR_INVALID_ARGUMENT;
+    int64_t s = 0;
+    for (int64_t h = 0; h < H; ++h)
+        for (int64_t c = 0; c < C; ++c) {
+            const int64_t s2 = std::min(need, s + q[h * C + c]);
+            const double nxt = at(h + 1, s2);
+            if (nxt != NEG && (double)perf[h * C + c] + nxt == at(h, s)) {
+                choice[h] = (int32_t)c;
+                s = s2;
+                break;
+            }
+        }
     return VECATTN_OK;
 }
 

@@ -71,6 +71,8 @@ def load(path: str = LIB_PATH):
         "vecattn_last_cuda_error": (ctypes.c_char_p, []),
         "vecattn_abi_version": (i32, []),
         "vecattn_kernel_timing": (i32, [i32]),
+        "vecattn_alpha_dp": (i32, [i32, i32, P(ctypes.c_float), P(ctypes.c_float), ctypes.c_float, i32, P(i32),
+                                   P(ctypes.c_double)]),
         "vecattn_select_naive_workspace_bytes": (sz, [prob, i32, i32]),
         "vecattn_select_naive": (i32, [prob, i32, i32, ctypes.c_float, ctypes.c_float, vp, vp, vp, vp, i64, vp, vp,
                                        sz, vp]),
@@ -89,7 +91,24 @@ EXPORTED = ["vecattn_pool", "vecattn_select_workspace_bytes", "vecattn_select", 
             "vecattn_forward_workspace_bytes", "vecattn_forward",
             "vecattn_validate_selection", "vecattn_debug_scores", "vecattn_status_string", "vecattn_last_cuda_error",
             "vecattn_abi_version", "vecattn_kernel_timing", "vecattn_kernel_timing_last",
-            "vecattn_select_naive_workspace_bytes", "vecattn_select_naive"]
+            "vecattn_select_naive_workspace_bytes", "vecattn_select_naive", "vecattn_alpha_dp"]
+
+
+def alpha_dp(sp, perf, rho_target: float, grid: int = 1000):
+    """Eq. 4 per-head filter-ratio search (host-only C ABI call, vecattn_alpha_dp).
+    sp, perf: array-likes [H, n_cand].  Returns (choice int32 [H], best total perf); raises
+    VecAttnError if no assignment reaches rho_target."""
+    import numpy as np
+    sp = np.ascontiguousarray(sp, np.float32)
+    perf = np.ascontiguousarray(perf, np.float32)
+    H, C = sp.shape
+    choice = np.zeros(H, np.int32)
+    best = ctypes.c_double()
+    rc = load().vecattn_alpha_dp(H, C, sp.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+                                 perf.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), float(rho_target), int(grid),
+                                 choice.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), ctypes.byref(best))
+    _check("vecattn_alpha_dp", rc)
+    return choice, best.value
 
 NAIVE_MINS = 0
 NAIVE_TOPP = 1
