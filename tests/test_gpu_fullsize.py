@@ -1,0 +1,75 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+Inputs are built by bench.build_inputs on the bench's workloads with bench's alpha. The
+workloads are dit128k (N = 131072, 24 heads, non-causal, the headline) and vlm128k
+(N = 131072, 28/4 heads, causal). One fused vecattn_forward produces the outputs, and the
+dense kernel is checked too.
+
+The oracle computes sampled outputs one at a time:
+  * selection: sampled pooled rows of several heads, Alg. 1 with the parity rule's near-tie
+    tolerance;
+  * attention: sampled query blocks (first, last, random) on the GPU's own index sets, at
+    the north-star tolerances;
+  * dense: sampled query rows.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as orc
+from paper_2603_29494_b200 import synth
+from tests.parity import ATOL_MAX, ATOL_MEAN, LSE_ATOL, bf16_np, compare_selection
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("wl_name,alpha", [("dit128k", 1.0039), ("vlm128k", None)])
+def test_full_size_forward_sampled(wl_name, alpha):
+    import bench
+    import paper_2603_29494_b200.vecattn as va
+    va.load()
+    wl = synth.WORKLOADS[wl_name]
+    dev = torch.device("cuda:0")
+    q, k, v = bench.build_inputs(wl, "video", dev, 0, wl.Hq)
+    pq = 64
+    Np = (wl.N + pq - 1) // pq
+    if alpha is None:  # calibrated like bench.py (global alpha for rho = 0.785)
+        from paper_2603_29494_b200 import calibrate as cal
+        alpha = cal.calibrate_uniform(q, k, va.SelectConfig(mode="alg1", pq=pq, gk=wl.gk), 0.785, causal=wl.causal)
+    cfg = va.SelectConfig(mode="alg1", pq=pq, bk=16, gk=wl.gk, alpha=alpha)
+    o, lse, off, idx = va.forward(q, k, v, cfg, causal=wl.causal)
+    qp = va.pool(q, pq)
+    torch.cuda.synchronize()
+    off_h, idx_h = off.cpu().numpy(), idx.cpu().numpy()
+    assert va.validate_selection(off, idx, tuple(q.shape), pq, wl.causal) == 0
+    rng = np.random.default_rng(5)
+    rep = wl.Hq // wl.Hkv
+    for h in (0, wl.Hq // 2, wl.Hq - 1):
+        kv = h // rep
+        kh = bf16_np(k[0, kv])
+        vh = bf16_np(v[0, kv])
+        qh = bf16_np(q[0, h])
+        # ---- selection on sampled pooled rows
+        rows = np.unique(np.concatenate([[0, Np - 1], rng.choice(Np, 6, replace=False)]))
+        n, nk, ties = compare_selection(off_h, idx_h, bf16_np(qp[0, h]), kh, pq, rows, causal=wl.causal,
+                                        mode=orc.SEL_MINS_ALG1, bk=16, gk=wl.gk, alpha=alpha, row_base=h * Np)
+        assert ties <= 4
+        # ---- attention on sampled blocks, on the GPU's own index sets
+        hoff = off_h[h * Np:(h + 1) * Np + 1] - off_h[h * Np]
+        hidx = idx_h[off_h[h * Np]:off_h[(h + 1) * Np]]
+        blocks = np.unique(np.concatenate([[0, Np - 1], rng.choice(Np, 3, replace=False)]))
+        oo, ol = orc.sparse_attn(qh, kh, vh, hoff, hidx, pq, causal=wl.causal, blocks=blocks)
+        rows_q = (blocks[:, None] * pq + np.arange(pq)[None, :]).reshape(-1)
+        ok = rows_q < wl.N
+        og = o[0, h].float().cpu().numpy()[rows_q[ok]]
+        err = np.abs(og - oo[ok])
+        assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN, (wl_name, h, err.max(), err.mean())
+        assert np.abs(lse[0, h].cpu().numpy()[rows_q[ok]] - ol[ok]).max() <= LSE_ATOL
+    # ---- dense kernel on sampled rows of one head
+    od, ld = va.dense_fwd(q[:, :1].contiguous(), k[:, :1].contiguous(), v[:, :1].contiguous(), causal=wl.causal)
+    torch.cuda.synchronize()
+    rows = np.unique(np.concatenate([[0, wl.N - 1], rng.choice(wl.N, 14, replace=False)]))
+    do, dl = orc.dense_attn(bf16_np(q[0, 0]), bf16_np(k[0, 0]), bf16_np(v[0, 0]), causal=wl.causal, rows=rows)
+    err = np.abs(od[0, 0].float().cpu().numpy()[rows] - do)
+    assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN, (wl_name, "dense", err.max(), err.mean())
+    assert np.abs(ld[0, 0].cpu().numpy()[rows] - dl).max() <= LSE_ATOL
