@@ -159,6 +159,11 @@ SPARSE_CASES = [
     ("video", 1, 2, 2, 5000, 128, 128, True, dict(mode="exact", alpha=1.2)),
     ("video", 1, 2, 1, 6000, 64, 64, False, dict(mode="alg1", alpha=1.5, gk=8192)),
     ("gauss", 2, 2, 2, 2000, 128, 64, True, dict(mode="topk", keep_frac=0.2)),
+    # kernel coverage: 128-key gather kernel at D=64 (causal), double-buffered kernel at
+    # P_q=128 and with B=2 (non-causal)
+    ("video", 1, 2, 1, 3000 + 40, 64, 64, True, dict(mode="alg1", alpha=1.2, gk=16)),
+    ("gauss", 1, 2, 2, 4096 + 40, 128, 128, False, dict(mode="alg1", alpha=0.3, gk=8192)),
+    ("video", 2, 2, 1, 3000, 128, 64, False, dict(mode="exact", alpha=1.4)),
 ]
 
 
