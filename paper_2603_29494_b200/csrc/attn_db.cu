@@ -34,6 +34,7 @@
 // LSE_r = scale*<q_r,k_r>.
 #include "common.cuh"
 #include "kernels.cuh"
+#include "attn_plan.cuh"
 
 #include <math.h>
 
@@ -78,95 +79,13 @@ struct AttnCfg {
 
 VA_DEV uint32_t s_col(int t, int b) { return 256u + 128u * t + 64u * b; }
 
-// Debug timeline (p.trace != null): CTA 0 records clock64() per chunk and event kind
-// (0 K issue, 1 V issue, 2 K landed, 3 V landed, 4/5 PV0/PV1 issued, 6/7 S0 ready/P0 done,
-// 8/9 S1 ready/P1 done) -- scripts/trace_run.py.
-constexpr int kTraceChunks = 4096;
-VA_DEV void trace(const AttnParams& p, int kind, int64_t c) {
-    if (p.trace != nullptr && blockIdx.x == 0 && c < kTraceChunks)
-        p.trace[(int64_t)kind * kTraceChunks + c] = clock64();
-}
-
-struct Item {
-    int64_t bh, it;  // head, 256-row item within the head
-    int n_chunks;
-    int lb, l0, l1;  // gather: plan segment lengths (keys of both tiles | tile 0 only | tile 1 only)
-    int nb, n0, n1;  // gather: chunks per segment
-    int len;         // dense: key extent
-    int64_t base;    // gather: plan base
-};
-
-struct Chunk {
-    int mask;   // bit t: tile t computes this chunk
-    int start;  // first plan entry (relative to the item base) / first key (dense)
-    int len;    // valid entries / keys
-};
-
-template <bool GATHER>
-VA_DEV Item decode_item(const AttnParams& p, int item) {
-    Item I;
-    I.bh = item / p.n_mt;
-    I.it = p.n_mt - 1 - (item % p.n_mt);  // longest-first within a head (causal)
-    if constexpr (GATHER) {
-        const int64_t G = 256 / p.pq;
-        const int64_t x = I.bh * p.n_mt + I.it;
-        I.lb = p.wl_len[3 * x];
-        I.l0 = p.wl_len[3 * x + 1];
-        I.l1 = p.wl_len[3 * x + 2];
-        I.nb = (I.lb + kChunk - 1) / kChunk;
-        I.n0 = (I.l0 + kChunk - 1) / kChunk;
-        I.n1 = (I.l1 + kChunk - 1) / kChunk;
-        I.n_chunks = I.nb + I.n0 + I.n1;
-        I.base = p.offsets[I.bh * p.Np + G * I.it];
-        I.len = 0;
-    } else {
-        const int64_t kend = p.causal ? min(p.N, (I.it + 1) * 256) : p.N;
-        I.len = (int)kend;
-        I.base = 0;
-        I.n_chunks = (int)((kend + kChunk - 1) / kChunk);
-        I.lb = I.l0 = I.l1 = I.nb = I.n0 = I.n1 = 0;
-    }
-    return I;
-}
-
-// Chunk order: shared chunks first, then tile-0-only and tile-1-only chunks interleaved
-// (so the tensor core alternates between the two softmax warpgroups).
-template <bool GATHER>
-VA_DEV Chunk chunk_info(const Item& I, int j) {
-    Chunk c;
-    if constexpr (!GATHER) {
-        c.mask = 3;
-        c.start = kChunk * j;
-        c.len = min(kChunk, I.len - kChunk * j);
-        return c;
-    } else {
-        if (j < I.nb) {
-            c.mask = 3;
-            c.start = kChunk * j;
-            c.len = min(kChunk, I.lb - kChunk * j);
-            return c;
-        }
-        const int k = j - I.nb;
-        const int m = min(I.n0, I.n1);
-        int t, q;
-        if (k < 2 * m) {
-            t = k & 1;
-            q = k >> 1;
-        } else {
-            t = I.n0 > I.n1 ? 0 : 1;
-            q = m + (k - 2 * m);
-        }
-        c.mask = 1 << t;
-        if (t == 0) {
-            c.start = I.lb + kChunk * q;
-            c.len = min(kChunk, I.l0 - kChunk * q);
-        } else {
-            c.start = I.lb + I.l0 + kChunk * q;
-            c.len = min(kChunk, I.l1 - kChunk * q);
-        }
-        return c;
-    }
-}
+using plan::Chunk;
+using plan::Item;
+using plan::trace;
+template <bool G>
+VA_DEV Item decode_item(const AttnParams& p, int item) { return plan::decode_item<kChunk, G>(p, item); }
+template <bool G>
+VA_DEV Chunk chunk_info(const Item& I, int j) { return plan::chunk_info<kChunk, G>(I, j); }
 
 VA_DEV uint32_t prefix_mask(int64_t nb) { return nb >= 32 ? 0xffffffffu : (nb <= 0 ? 0u : ((1u << nb) - 1u)); }
 

@@ -1,0 +1,133 @@
+// attn_plan.cuh — walking an attention item's key plan, shared by the two attention
+// kernels (attn.cu, attn_db.cu).  Internal to the library; no oracle code.
+//
+// A work item is 256 query rows (two M=128 tiles) of one head.  Its plan (built by
+// plan_kernel / worklist_kernel) is the union of the item's block index lists in three
+// sorted segments -- keys of both tiles, tile 0 only, tile 1 only -- cut into chunks of
+// CHUNK keys; the dense path walks contiguous key chunks instead.
+#pragma once
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace va {
+namespace plan {
+
+// Debug timeline (p.trace != null): CTA 0 records clock64() per chunk and event kind
+// (0 K issue, 1 V issue, 2 K landed, 3 V landed, 4/5 PV0/PV1 issued, 6/7 S0 ready/P0 done,
+// 8/9 S1 ready/P1 done) -- scripts/trace_run.py.
+constexpr int kTraceChunks = 4096;
+VA_DEV void trace(const AttnParams& p, int kind, int64_t c) {
+    if (p.trace != nullptr && blockIdx.x == 0 && c < kTraceChunks)
+        p.trace[(int64_t)kind * kTraceChunks + c] = clock64();
+}
+
+struct Item {
+    int64_t bh, it;  // head, 256-row item within the head
+    int n_chunks;
+    int lb, l0, l1;  // gather: plan segment lengths (keys of both tiles | tile 0 only | tile 1 only)
+    int nb, n0, n1;  // gather: chunks per segment
+    int len;         // dense: key extent
+    int64_t base;    // gather: plan base
+};
+
+struct Chunk {
+    int mask;   // bit t: tile t computes this chunk
+    int start;  // first plan entry (relative to the item base) / first key (dense)
+    int len;    // valid entries / keys
+};
+
+template <int kChunk, bool GATHER>
+VA_DEV Item decode_item(const AttnParams& p, int item) {
+    Item I;
+    I.bh = item / p.n_mt;
+    I.it = p.n_mt - 1 - (item % p.n_mt);  // longest-first within a head (causal)
+    if constexpr (GATHER) {
+        const int64_t G = 256 / p.pq;
+        const int64_t x = I.bh * p.n_mt + I.it;
+        I.lb = p.wl_len[3 * x];
+        I.l0 = p.wl_len[3 * x + 1];
+        I.l1 = p.wl_len[3 * x + 2];
+        I.nb = (I.lb + kChunk - 1) / kChunk;
+        I.n0 = (I.l0 + kChunk - 1) / kChunk;
+        I.n1 = (I.l1 + kChunk - 1) / kChunk;
+        I.n_chunks = I.nb + I.n0 + I.n1;
+        I.base = p.offsets[I.bh * p.Np + G * I.it];
+        I.len = 0;
+    } else {
+        const int64_t kend = p.causal ? min(p.N, (I.it + 1) * 256) : p.N;
+        I.len = (int)kend;
+        I.base = 0;
+        I.n_chunks = (int)((kend + kChunk - 1) / kChunk);
+        I.lb = I.l0 = I.l1 = I.nb = I.n0 = I.n1 = 0;
+    }
+    return I;
+}
+
+// Chunk order: shared chunks first, then tile-0-only and tile-1-only chunks interleaved
+// (so the tensor core alternates between the two softmax warpgroups).
+template <int kChunk, bool GATHER>
+VA_DEV Chunk chunk_info(const Item& I, int j) {
+    Chunk c;
+    if constexpr (!GATHER) {
+        c.mask = 3;
+        c.start = kChunk * j;
+        c.len = min(kChunk, I.len - kChunk * j);
+        return c;
+    } else {
+        if (j < I.nb) {
+            c.mask = 3;
+            c.start = kChunk * j;
+            c.len = min(kChunk, I.lb - kChunk * j);
+            return c;
+        }
+        const int k = j - I.nb;
+        const int m = min(I.n0, I.n1);
+        int t, q;
+        if (k < 2 * m) {
+            t = k & 1;
+            q = k >> 1;
+        } else {
+            t = I.n0 > I.n1 ? 0 : 1;
+            q = m + (k - 2 * m);
+        }
+        c.mask = 1 << t;
+        if (t == 0) {
+            c.start = I.lb + kChunk * q;
+            c.len = min(kChunk, I.l0 - kChunk * q);
+        } else {
+            c.start = I.lb + I.l0 + kChunk * q;
+            c.len = min(kChunk, I.l1 - kChunk * q);
+        }
+        return c;
+    }
+}
+
+// First chunk index > j that tile t computes (n_chunks if none).
+template <bool GATHER>
+VA_DEV int next_chunk(const Item& I, int t, int j) {
+    if constexpr (!GATHER) {
+        return j + 1;
+    } else {
+        const int n = I.n_chunks;
+        const int mt = t == 0 ? I.n0 : I.n1;
+        const int m = min(I.n0, I.n1);
+        int x = j + 1;
+        if (x < I.nb) return x;
+        if (mt == 0) return n;
+        // own chunks of tile t after the shared segment: interleaved k = 2q + t (q < m), then
+        // (if t owns the longer list) the tail k >= 2m
+        const int k = x - I.nb;
+        if (k < 2 * m) {
+            const int kk = ((k & 1) == t) ? k : k + 1;
+            if (kk < 2 * m) return I.nb + kk;
+            // past the interleave: the tail belongs to tile t only if its list is the longer
+        }
+        const bool tail_owner = (t == 0) ? (I.n0 > I.n1) : (I.n1 >= I.n0);
+        if (!tail_owner || mt == m) return n;
+        return max(x, I.nb + 2 * m);
+    }
+}
+
+}  // namespace plan
+}  // namespace va
