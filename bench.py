@@ -220,6 +220,12 @@ def build_inputs(wl, kind, dev, h0, h1):
                 else:
                     q[b, hq - h0] = torch.randn(N, D, generator=g, device=dev).to(torch.bfloat16)
             del dirs
+    if rep > 1 and (h0 % rep != 0 or (h1 - h0) % rep != 0):
+        # head range not aligned with KV groups (e.g. 28 heads over 8 ranks): give every
+        # local query head its own copy of its KV head so the ABI's GQA mapping (local head
+        # h reads KV head h / (Hq/Hkv)) stays exact
+        sel = torch.tensor([hq // rep - kv0 for hq in range(h0, h1)], device=dev)
+        k, v = k.index_select(1, sel).contiguous(), v.index_select(1, sel).contiguous()
     return q, k, v
 
 # ---------------------------------------------------------------------------- ours
@@ -410,14 +416,39 @@ def run_ours(args):
         vh.copy_(v)
         qd, kd, vd = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
 
+        # Host copies overlap the compute: the local heads run as up to 4 KV-head groups;
+        # group g's H2D (copy stream) runs while group g-1 computes, and (one rank) group
+        # g-1's output D2H (second copy stream) while group g computes.
+        nkv, nq = k.shape[1], q.shape[1]
+        rep_l = nq // nkv
+        n_ch = min(4, nkv) if B == 1 else 1
+        cb = [round(i * nkv / n_ch) for i in range(n_ch + 1)]
+        chunks = [(cb[i] * rep_l, cb[i + 1] * rep_l, cb[i], cb[i + 1]) for i in range(n_ch)]
+        s_h2d, s_d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+
         def e2e_step():
-            qd.copy_(qh, non_blocking=True)
-            kd.copy_(kh, non_blocking=True)
-            vd.copy_(vh, non_blocking=True)
-            va.forward_into(qd, kd, vd, cfg, offsets, indices, cap, d_nnz, cap, o, lse, ws_fwd, causal)
+            s_h2d.wait_stream(stream)
+            for (q0, q1, k0, k1) in chunks:
+                with torch.cuda.stream(s_h2d):
+                    qd[:, q0:q1].copy_(qh[:, q0:q1], non_blocking=True)
+                    kd[:, k0:k1].copy_(kh[:, k0:k1], non_blocking=True)
+                    vd[:, k0:k1].copy_(vh[:, k0:k1], non_blocking=True)
+                    ev_in = torch.cuda.Event()
+                    ev_in.record(s_h2d)
+                stream.wait_event(ev_in)
+                va.forward_into(qd[:, q0:q1], kd[:, k0:k1], vd[:, k0:k1], cfg, offsets, indices, cap, d_nnz, cap,
+                                o[:, q0:q1], lse[:, q0:q1], ws_fwd, causal)
+                if ws == 1:
+                    ev_out = torch.cuda.Event()
+                    ev_out.record(stream)
+                    with torch.cuda.stream(s_d2h):
+                        s_d2h.wait_event(ev_out)
+                        oh_host[:, q0:q1].copy_(o[:, q0:q1], non_blocking=True)
             if ws > 1:
                 allgather_heads(o, o_pad, o_all)
-            oh_host.copy_(o_all if ws > 1 else o, non_blocking=True)
+                oh_host.copy_(o_all, non_blocking=True)
+            else:
+                stream.wait_stream(s_d2h)
 
         e2e_step()
         torch.cuda.synchronize()
