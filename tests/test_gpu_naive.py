@@ -44,6 +44,7 @@ CASES = [  # kind, B, Hq, Hkv, N, D, pq, causal, alpha
     ("video", 1, 2, 1, 4096, 128, 64, True, 1.2),
     ("gauss", 2, 2, 1, 3000, 64, 128, False, 0.3),
     ("video", 1, 3, 3, 1024 + 16, 128, 64, True, 0.9),
+    ("gauss", 1, 1, 1, 1024 + 3, 128, 64, False, 0.3),   # N % 4 != 0: scalar paths of the filters
 ]
 
 
@@ -70,6 +71,7 @@ TOPP_CASES = [  # kind, B, Hq, Hkv, N, D, pq, causal, p
     ("video", 1, 2, 1, 4096, 128, 64, False, 0.5),
     ("video", 1, 2, 1, 4096 + 40, 128, 64, True, 0.9),
     ("gauss", 1, 1, 1, 3000, 64, 128, True, 0.7),
+    ("gauss", 1, 1, 1, 1024 + 3, 128, 64, False, 0.8),   # N % 4 != 0
 ]
 
 
