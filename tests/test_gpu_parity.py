@@ -164,6 +164,10 @@ SPARSE_CASES = [
     ("video", 1, 2, 1, 3000 + 40, 64, 64, True, dict(mode="alg1", alpha=1.2, gk=16)),
     ("gauss", 1, 2, 2, 4096 + 40, 128, 128, False, dict(mode="alg1", alpha=0.3, gk=8192)),
     ("video", 2, 2, 1, 3000, 128, 64, False, dict(mode="exact", alpha=1.4)),
+    # tiny / ragged problems: one partial item, last block of 1 row
+    ("gauss", 1, 1, 1, 65, 128, 64, False, dict(mode="alg1", alpha=0.5, gk=16)),
+    ("gauss", 1, 2, 1, 100, 64, 64, True, dict(mode="alg1", alpha=0.5, gk=16)),
+    ("gauss", 1, 1, 1, 200, 128, 128, True, dict(mode="topk", keep_frac=0.5)),
 ]
 
 
