@@ -20,6 +20,7 @@ using va::AttnParams;
 using va::SelectParams;
 
 constexpr size_t kAlign = 256;
+constexpr int64_t kMaxSplit = 8;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -106,6 +107,7 @@ struct SelectWs {
     uint32_t* bitmask;
     unsigned long long* counts;
     uint32_t* rowmax;
+    uint32_t* segmax;
     uint32_t* tk_prefix;
     uint32_t* tk_krem;
     size_t total;
@@ -124,6 +126,8 @@ SelectWs carve_select(const vecattn_problem_t* p, int32_t pq, void* base) {
     off += align_up((size_t)R * 8);
     w.rowmax = reinterpret_cast<uint32_t*>(b + off);
     off += align_up((size_t)R * 4);
+    w.segmax = reinterpret_cast<uint32_t*>(b + off);
+    off += align_up((size_t)R * kMaxSplit * 4);
     w.tk_prefix = reinterpret_cast<uint32_t*>(b + off);
     off += align_up((size_t)R * 4);
     w.tk_krem = reinterpret_cast<uint32_t*>(b + off);
@@ -133,6 +137,27 @@ SelectWs carve_select(const vecattn_problem_t* p, int32_t pq, void* base) {
 }
 
 int64_t gcd64(int64_t a, int64_t b) { return b == 0 ? a : gcd64(b, a % b); }
+
+// ALG1 K-split.  With G_K * B_K >= N (DiT: one Alg. 1 group per row) a row is
+// one sequential unit, so few heads per GPU leave SMs idle (3 heads at 8 GPUs = 48 row tiles
+// for 148 SMs).  Then split rows into up to kMaxSplit key segments: a max pass writes each
+// segment's row max, and the ALG1 pass starts segment s at the max of segments < s, which is
+// exactly the running max Alg. 1 carries into the segment.  Returns the segment count (1 = no
+// split).  VECATTN_SELECT_SPLIT=<n> forces n (tests).
+int select_split(const vecattn_problem_t* p, const vecattn_select_params_t* s, int64_t units) {
+    const int64_t G = (int64_t)s->bk * (int64_t)s->gk;
+    if (s->mode != VECATTN_SEL_MINS_ALG1 || p->causal || G < p->N) return 1;
+    int n = 1;
+    if (const char* env = getenv("VECATTN_SELECT_SPLIT")) n = atoi(env);
+    else {
+        int dev = 0, sms = va::kNumSMsB200;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (units < sms) n = (int)((sms + units - 1) / units);  // fill one wave
+    }
+    n = std::max(1, std::min(n, (int)kMaxSplit));
+    const int64_t nblk = (p->N + 255) / 256;  // segments are multiples of the 256-key tile
+    return (int)std::min<int64_t>(n, nblk);
+}
 
 // Keys per CTA unit.  Units never split a G_K group (Alg. 1 running max scope), so a
 // segment is a multiple of lcm(B_K*G_K, 256); TOPK needs whole rows.
@@ -171,6 +196,7 @@ vecattn_status_t fill_select_params(const vecattn_problem_t* p, const vecattn_se
     sp.bitmask = w.bitmask;
     sp.counts = w.counts;
     sp.rowmax = w.rowmax;
+    sp.segmax = w.segmax;
     sp.tk_prefix = w.tk_prefix;
     sp.tk_krem = w.tk_krem;
     sp.topk = s ? s->topk : 0;
@@ -203,8 +229,16 @@ vecattn_status_t cuda_status(cudaError_t e) {
 cudaError_t run_select(const vecattn_problem_t* p, const vecattn_select_params_t* s, const void* q, const void* k,
                        int64_t* offsets, int64_t* d_nnz, const SelectWs& w, SelectParams& sp, cudaStream_t cs) {
     const int64_t R = sp.BH * sp.Np;
+    const int nsplit = select_split(p, s, sp.BH * sp.n_mt);
     auto run = [&](int epi, int pass) -> cudaError_t {
         plan_segments(p, s, epi, sp);
+        sp.split = 0;
+        if (nsplit > 1 && (epi == va::EPI_ALG1 || epi == va::EPI_MAX)) {
+            const int64_t nblk = (p->N + 255) / 256;
+            sp.seg_len = (nblk + nsplit - 1) / nsplit * 256;
+            sp.n_seg = (p->N + sp.seg_len - 1) / sp.seg_len;
+            sp.split = 1;
+        }
         sp.pass = pass;
         if (set_k_map(p, k, epi == va::EPI_TOPK_HIST ? 128 : 256, sp) != VECATTN_OK) return cudaErrorInvalidValue;
         return va::launch_select(sp, epi, (int)p->D, cs);
@@ -213,7 +247,8 @@ cudaError_t run_select(const vecattn_problem_t* p, const vecattn_select_params_t
     if (e == cudaSuccess) e = cudaMemsetAsync(w.counts, 0, (size_t)R * 8, cs);
     if (e == cudaSuccess) {
         if (s->mode == VECATTN_SEL_MINS_ALG1) {
-            e = run(va::EPI_ALG1, 0);
+            if (nsplit > 1) e = run(va::EPI_MAX, 0);  // per-segment row maxima (split)
+            if (e == cudaSuccess) e = run(va::EPI_ALG1, 0);
         } else if (s->mode == VECATTN_SEL_MINS_EXACT) {
             e = cudaMemsetAsync(w.rowmax, 0, (size_t)R * 4, cs);
             if (e == cudaSuccess) e = run(va::EPI_MAX, 0);

@@ -38,6 +38,9 @@ struct SelectParams {
     uint32_t* bitmask;             // [BH*Np, words_per_row]
     unsigned long long* counts;    // [BH*Np]
     uint32_t* rowmax;              // [BH*Np] ordered keys (EXACT)
+    uint32_t* segmax;              // [BH*Np][n_seg] ordered keys: per-segment row max (split ALG1)
+    int32_t split;                 // ALG1 K-split: EPI_MAX writes segmax; EPI_ALG1 starts
+                                   // each segment's running max at the max of the earlier segments
     uint32_t* tk_prefix;           // [BH*Np] TOPK radix state
     uint32_t* tk_krem;             // [BH*Np]
     float* scores_out;             // EPI_SCORES: [BH*Np, N] fp32 (debug)

@@ -165,6 +165,14 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
         const int64_t G = (int64_t)p.bk * (int64_t)p.gk;
         int64_t next_reset = k_begin;              // Alg. 1 group boundaries (multiples of G)
         float m_run = -INFINITY;                   // ALG1 running max / EPI_MAX row max
+        if (EPI == EPI_ALG1 && p.split && row_ok) {
+            // K-split of a single-group row (G >= N): this segment continues the group that
+            // started at key 0, so the running max starts at the max of the earlier segments
+            // (Alg. 1's m_S is the max over every earlier visible key of the group).
+            for (int64_t s2 = 0; s2 < seg; ++s2)
+                m_run = fmaxf(m_run, f32_from_order_key(p.segmax[grow * p.n_seg + s2]));
+            next_reset = (k_begin + G - 1) / G * G;
+        }
         float thr_fixed = 0.f;
         uint32_t tk_prefix = 0, tk_krem = 0, tk_taken = 0;
         unsigned long long cnt = 0;
@@ -319,7 +327,8 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
             if constexpr (EPI == EPI_ALG1 || EPI == EPI_THRESH || EPI == EPI_TOPK_EMIT) {
                 if (cnt) atomicAdd(&p.counts[grow], cnt);
             } else if constexpr (EPI == EPI_MAX) {
-                if (m_run > -INFINITY) atomicMax(&p.rowmax[grow], f32_order_key(m_run));
+                if (p.split) p.segmax[grow * p.n_seg + seg] = f32_order_key(m_run);
+                else if (m_run > -INFINITY) atomicMax(&p.rowmax[grow], f32_order_key(m_run));
             } else if constexpr (EPI == EPI_TOPK_HIST) {
                 // find the bin holding the krem-th largest remaining key (scan from the top)
                 uint32_t cum = 0;

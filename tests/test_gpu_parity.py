@@ -280,3 +280,19 @@ def test_fused_forward_capacity_protocol():
     assert n > small and bool((o == 7.0).all())   # plan capacity too small: attention skipped
     o2, lse2, off2, idx2 = va.forward(qd, kd, vd, cfg, nnz_cap=small)  # binding retries with nnz
     assert idx2.numel() == n
+
+
+@pytest.mark.parametrize("nsplit", [2, 3, 8])
+def test_alg1_k_split_equals_sequential(nsplit, monkeypatch):
+    """a single-group ALG1 row split into key segments (segment maxima, then each
+    segment starts from the max of the earlier ones) gives exactly the sequential result."""
+    q, k, v, qd, kd, vd = make("video", 1, 2, 1, 4096 + 300, 128)
+    cfg = va.SelectConfig(mode="alg1", pq=64, gk=8192, alpha=1.1)
+    monkeypatch.setenv("VECATTN_SELECT_SPLIT", "1")
+    off1, idx1 = va.select(qd, kd, cfg)
+    monkeypatch.setenv("VECATTN_SELECT_SPLIT", str(nsplit))
+    off2, idx2 = va.select(qd, kd, cfg)
+    o2, lse2, off3, idx3 = va.forward(qd, kd, vd, cfg)
+    torch.cuda.synchronize()
+    assert torch.equal(off1, off2) and torch.equal(idx1, idx2)
+    assert torch.equal(off1, off3) and torch.equal(idx1, idx3)
