@@ -174,6 +174,17 @@ void plan_segments(const vecattn_problem_t* p, const vecattn_select_params_t* s,
         seg = 16384;
     }
     if (seg > Nr) seg = Nr;
+    // few rows (e.g. one GPU's share of the heads): shorter segments until the units fill
+    // two waves, keeping segments a multiple of the unit granule and >= 2048 keys
+    const int64_t granule = (epi == va::EPI_ALG1 && (int64_t)s->bk * s->gk < p->N)
+                                ? (int64_t)s->bk * s->gk / gcd64((int64_t)s->bk * s->gk, 256) * 256
+                                : 256;
+    const int64_t row_units = sp.BH * sp.n_mt;
+    if (epi == va::EPI_ALG1 || epi == va::EPI_MAX || epi == va::EPI_THRESH) {
+        while (row_units * ((p->N + seg - 1) / seg) < 2 * va::kNumSMsB200 && seg / 2 >= 2048 &&
+               (seg / 2) % granule == 0 && (epi != va::EPI_ALG1 || (int64_t)s->bk * s->gk < p->N))
+            seg /= 2;
+    }
     sp.seg_len = seg;
     sp.n_seg = (p->N + seg - 1) / seg;
 }
