@@ -365,6 +365,16 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     step_ms = float(tt[0]) / args.steps
 
+    # ---- warm-L2 step time (no flush between steps; SURVEY 8(d) reports both)
+    torch.cuda.synchronize()
+    ew0, ew1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ew0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ew1.record(stream)
+    torch.cuda.synchronize()
+    warm_ms = ew0.elapsed_time(ew1) / args.steps
+
     # ---- stage breakdown via the two-call C ABI path (vecattn_select + vecattn_sparse_fwd)
     ws_sp = torch.empty(va.sparse_workspace_bytes(pr, pq, cap), dtype=torch.uint8, device=dev)
     brk = []
@@ -519,6 +529,7 @@ def run_ours(args):
                    "nnz": int(sp_tot[1]), "parallelism": f"head-parallel x{ws}" + (" + NCCL all-gather(O)" if ws > 1 else ""),
                    "l2": "256 MB L2 flush between timed steps; inputs (2.4 GB) >> L2"},
         "forward_ms": round(float(tt[1]) / args.steps, 4),
+        "step_ms_warm_l2": round(warm_ms, 4),
         "allgather_ms": round(float(tt[2]) / args.steps, 4) if ws > 1 else 0.0,
         "breakdown_two_call": {"select_ms": round(sel_ms_avg, 4), "sparse_fwd_ms": round(sparse_ms_avg, 4),
                                "note": "vecattn_select + vecattn_sparse_fwd (CSR round trip), L2-flushed"},
