@@ -390,13 +390,24 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                     const int s = (int)(c % S_);
                     const bool more = j + 1 < I.n_chunks;
                     int mn = 0;
-                    if (more) {
+                    auto issue_next_s = [&]() {
                         mn = chunk_info<GATHER>(I, j + 1).mask;
-                        wait_k(c + 1);
                         if (mn & 1) issue_s(0, c + 1);
                         if (mn & 2) issue_s(1, c + 1);
                         mma_commit(&bars[C::B_KEMPTY + (int)((c + 1) % S_)]);
                         if (j + 2 == I.n_chunks) mma_commit(&bars[C::B_QEMPTY]);
+                    };
+                    // S(j+1) first if its K chunk has landed (softmax(j+1) can then overlap
+                    // PV(j)); otherwise PV(j) first so the tensor core does not idle on the gather
+                    bool s_first = false;
+                    if (more) {
+                        const int64_t cn = c + 1;
+                        s_first = mbar_try_wait(&bars[C::B_KFULL + (int)(cn % S_)], (uint32_t)((cn / S_) & 1));
+                        if (s_first) {
+                            tc_fence_after();
+                            trace(p, 2, cn);
+                            issue_next_s();
+                        }
                     }
                     mbar_wait(&bars[C::B_VFULL + s], (uint32_t)((c / S_) & 1));
                     trace(p, 3, c);
@@ -408,6 +419,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                         trace(p, 4 + t, c);
                     }
                     mma_commit(&bars[C::B_VEMPTY + s]);
+                    if (more && !s_first) {
+                        wait_k(c + 1);
+                        issue_next_s();
+                    }
                     m = mn;
                 }
                 // O_0 / O_1 final for this item (one phase per item with chunks, both tiles)
