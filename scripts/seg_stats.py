@@ -34,3 +34,8 @@ print(f"chunks gathered: seg={(ch(lb)+ch(l0)+ch(l1)).sum()} pair={(ch(lb+l0)+ch(
 m = np.minimum(ch(l0), ch(l1))
 tail = np.abs(ch(l0) - ch(l1))
 print(f"128-key chunks: shared={ch(lb).sum()} interleaved-pairs={2*m.sum()} single-tile tail={tail.sum()}")
+# 64-key chunk accounting for the double-buffered kernel (tile-chunk = 128 rows x 64 keys)
+tc64 = (2 * ch64(lb) + ch64(l0) + ch64(l1)).sum()
+g64 = (ch64(lb) + ch64(l0) + ch64(l1)).sum()
+useful_rows_keys = nnz * 64
+print(f"64-key: tile-chunks={tc64} chunks gathered={g64} useful fraction of tile-chunk work={useful_rows_keys / (tc64 * 128 * 64):.3f}")

@@ -44,3 +44,7 @@ print("  V_landed->PV0_issued:", st(d(3, 4)))
 print("chunk period (K_landed[c+1]-K_landed[c]):", st(per))
 issue = np.diff(np.array([t[0, c] for c in range(n)]))
 print("K issue period:", st(issue))
+print("K issue duration (K_issue->K_issue_end):", st(d(0, 10)))
+print("V issue duration (V_issue->V_issue_end):", st(d(1, 11)))
+print("K issue_end->landed:", st(d(10, 2)))
+print("V issue_end->landed:", st(d(11, 3)))
