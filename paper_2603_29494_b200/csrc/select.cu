@@ -245,42 +245,83 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
                         for (int j = 0; j < 64; ++j)
                             if (j >= nvis) v[j] = -INFINITY;
                     }
+                    // rowmax of every B_K sub-tile first (independent chains), then Alg. 1's
+                    // sequential running max and threshold per sub-tile
+                    float gmx[64 / BK];
+#pragma unroll
+                    for (int g = 0; g < 64 / BK; ++g) {
+                        float a = -INFINITY, b = -INFINITY;
+#pragma unroll
+                        for (int j = 0; j < BK; j += 4) {
+                            a = fmax3(a, v[g * BK + j], v[g * BK + j + 1]);
+                            b = fmax3(b, v[g * BK + j + 2], v[g * BK + j + 3]);
+                        }
+                        gmx[g] = fmaxf(a, b);
+                    }
+                    // keep = s >= m_S - alpha (R1) <=> the sign bit of s - thr is clear:
+                    // for finite thr the IEEE difference is negative exactly when s < thr (no
+                    // underflow to -0 with gradual underflow; s = -inf gives -inf).  The sign
+                    // bits are shifted in (funnel shift) and inverted/bit-reversed per word.
+                    uint32_t sg0 = 0u, sg1 = 0u;
 #pragma unroll
                     for (int sub = 0; sub < 64; sub += BK) {
                         if (kc + sub == next_reset) {  // new group of G_K tiles: m_S <- -inf
                             m_run = -INFINITY;
                             next_reset += G;
                         }
-                        float mx = -INFINITY;
+                        m_run = fmaxf(m_run, gmx[sub / BK]);      // m_S <- max(m_S, rowmax(S_tile))
+                        const float nthr = alpha_raw - m_run;     // -(m_S - alpha)
 #pragma unroll
-                        for (int j = 0; j < BK; j += 2) mx = fmax3(mx, v[sub + j], v[sub + j + 1]);
-                        m_run = fmaxf(m_run, mx);                 // m_S <- max(m_S, rowmax(S_tile))
-                        const float thr = m_run - alpha_raw;      // M <- S >= m_S - alpha (R1)
-                        if (nvis >= 64) {
-#pragma unroll
-                            for (int j = sub; j < sub + BK; ++j) {
-                                const uint32_t keep = v[j] >= thr ? 1u : 0u;
-                                if (j < 32) w0 |= keep << j;
-                                else w1 |= keep << (j - 32);
-                            }
-                        } else {
-#pragma unroll
-                            for (int j = sub; j < sub + BK; ++j) {
-                                const uint32_t keep = (j < nvis) && (v[j] >= thr) ? 1u : 0u;
-                                if (j < 32) w0 |= keep << j;
-                                else w1 |= keep << (j - 32);
+                        for (int j = sub; j < sub + BK; j += 2) {
+                            const float2 d = fadd2(make_float2(v[j], v[j + 1]), make_float2(nthr, nthr));
+                            if (j < 32) {
+                                sg0 = __funnelshift_l(__float_as_uint(d.x), sg0, 1);
+                                sg0 = __funnelshift_l(__float_as_uint(d.y), sg0, 1);
+                            } else {
+                                sg1 = __funnelshift_l(__float_as_uint(d.x), sg1, 1);
+                                sg1 = __funnelshift_l(__float_as_uint(d.y), sg1, 1);
                             }
                         }
                     }
+                    w0 = __brev(~sg0);
+                    w1 = __brev(~sg1);
+                    if (nvis < 64) {  // invisible keys (causal / ragged tail / row past N_p)
+                        w0 &= nvis >= 32 ? 0xffffffffu : ((1u << nvis) - 1u);
+                        w1 &= nvis >= 64 ? 0xffffffffu : (nvis <= 32 ? 0u : ((1u << (nvis - 32)) - 1u));
+                    }
                 } else if constexpr (EPI == EPI_MAX) {
+                    if (nvis < 64) {
 #pragma unroll
-                    for (int j = 0; j < 64; ++j)
-                        if (j < nvis) m_run = fmaxf(m_run, v[j]);
+                        for (int j = 0; j < 64; ++j)
+                            if (j >= nvis) v[j] = -INFINITY;
+                    }
+                    float a = -INFINITY, b = -INFINITY, c2 = -INFINITY, d2 = -INFINITY;  // 4 chains
+#pragma unroll
+                    for (int j = 0; j < 64; j += 8) {
+                        a = fmax3(a, v[j], v[j + 1]);
+                        b = fmax3(b, v[j + 2], v[j + 3]);
+                        c2 = fmax3(c2, v[j + 4], v[j + 5]);
+                        d2 = fmax3(d2, v[j + 6], v[j + 7]);
+                    }
+                    m_run = fmaxf(m_run, fmaxf(fmaxf(a, b), fmaxf(c2, d2)));
                 } else if constexpr (EPI == EPI_THRESH) {
+                    // keep = s >= thr <=> sign bit of s - thr clear (see EPI_ALG1)
+                    const float nthr = -thr_fixed;
+                    uint32_t sg0 = 0u, sg1 = 0u;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        w0 |= ((j < nvis) && (v[j] >= thr_fixed) ? 1u : 0u) << j;
-                        w1 |= ((j + 32 < nvis) && (v[j + 32] >= thr_fixed) ? 1u : 0u) << j;
+                    for (int j = 0; j < 32; j += 2) {
+                        const float2 d0 = fadd2(make_float2(v[j], v[j + 1]), make_float2(nthr, nthr));
+                        const float2 d1 = fadd2(make_float2(v[32 + j], v[32 + j + 1]), make_float2(nthr, nthr));
+                        sg0 = __funnelshift_l(__float_as_uint(d0.x), sg0, 1);
+                        sg0 = __funnelshift_l(__float_as_uint(d0.y), sg0, 1);
+                        sg1 = __funnelshift_l(__float_as_uint(d1.x), sg1, 1);
+                        sg1 = __funnelshift_l(__float_as_uint(d1.y), sg1, 1);
+                    }
+                    w0 = __brev(~sg0);
+                    w1 = __brev(~sg1);
+                    if (nvis < 64) {
+                        w0 &= nvis >= 32 ? 0xffffffffu : ((1u << nvis) - 1u);
+                        w1 &= nvis >= 64 ? 0xffffffffu : (nvis <= 32 ? 0u : ((1u << (nvis - 32)) - 1u));
                     }
                 } else if constexpr (EPI == EPI_TOPK_HIST) {
                     const int pass = p.pass;
