@@ -70,8 +70,10 @@ __global__ void __launch_bounds__(kEmitWarps * 32) emit_kernel(const uint32_t* _
         const int64_t nwords = (vis + 31) / 32;
         const uint32_t* src = bitmask + row * words_per_row;
         int64_t out = offsets[row];
+        uint32_t next = lane < nwords ? __ldg(src + lane) : 0u;  // software-pipelined by one round
         for (int64_t w0 = 0; w0 < nwords; w0 += 32) {
-            uint32_t word = (w0 + lane < nwords) ? __ldg(src + w0 + lane) : 0u;
+            uint32_t word = next;
+            next = (w0 + 32 + lane < nwords) ? __ldg(src + w0 + 32 + lane) : 0u;
             const int pc = __popc(word);
             int incl = pc;
 #pragma unroll
@@ -80,12 +82,12 @@ __global__ void __launch_bounds__(kEmitWarps * 32) emit_kernel(const uint32_t* _
                 if (lane >= o) incl += n;
             }
             const int total = __shfl_sync(0xffffffffu, incl, 31);
-            int pos = incl - pc;
+            int pos = incl;  // bits are taken from the top: fill [incl - pc, incl) backwards
             const int32_t kbase = (int32_t)((w0 + lane) * 32);
             while (word) {
-                const int bit = __ffs(word) - 1;
-                stage[w][pos++] = kbase + bit;
-                word &= word - 1;
+                const int bit = 31 - __clz(word);
+                stage[w][--pos] = kbase + bit;
+                word ^= 1u << bit;
             }
             __syncwarp();
             for (int t = lane; t < total; t += 32) indices[out + t] = stage[w][t];
@@ -186,48 +188,72 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const uint32_t* __re
     __syncthreads();
     const int64_t base = offsets[r0];
     int64_t run[3] = {base, base + tot[0], base + tot[0] + tot[1]};
-    // pass 2: rounds of kPlanThreads words
+    // pass 2: rounds of kPlanThreads words.  The three segment counts of a word are packed in
+    // one 64-bit value (21 bits each; a round holds at most 8192 keys), so a single block scan
+    // places all three; the round's entries are staged segment after segment (the segments
+    // are disjoint, so at most 8192 entries) and written out coalesced.
+    __shared__ unsigned long long sh64[kPlanThreads / 32];
+    uint32_t nx[4];  // next round's words (software-pipelined by one round)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) nx[b] = (b < nb && tid < vwords[b]) ? __ldg(bitmask + (r0 + b) * words_per_row + tid) : 0u;
     for (int64_t x0 = 0; x0 < wmax; x0 += kPlanThreads) {
         const int64_t x = x0 + tid;
         uint32_t bw[4];
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
-            bw[b] = (b < nb && x < vwords[b]) ? __ldg(bitmask + (r0 + b) * words_per_row + x) : 0u;
+        for (int b = 0; b < 4; ++b) {
+            bw[b] = nx[b];
+            const int64_t xn = x + kPlanThreads;
+            nx[b] = (b < nb && xn < vwords[b]) ? __ldg(bitmask + (r0 + b) * words_per_row + xn) : 0u;
+        }
         const uint32_t u0 = quad ? (bw[0] | bw[1]) : bw[0];
         const uint32_t u1 = quad ? (bw[2] | bw[3]) : bw[1];
         const uint32_t seg[3] = {u0 & u1, u0 & ~u1, u1 & ~u0};
+        const unsigned long long cnt = (unsigned long long)__popc(seg[0]) |
+                                       ((unsigned long long)__popc(seg[1]) << 21) |
+                                       ((unsigned long long)__popc(seg[2]) << 42);
+        unsigned long long incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long n = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += n;
+        }
+        if (lane == 31) sh64[w] = incl;
+        __syncthreads();
+        unsigned long long before = 0, rtot = 0;
+#pragma unroll
+        for (int y = 0; y < kPlanThreads / 32; ++y) {
+            const unsigned long long t = sh64[y];
+            before += (y < w) ? t : 0ull;
+            rtot += t;
+        }
+        const unsigned long long excl = before + incl - cnt;
+        constexpr unsigned long long F = (1ull << 21) - 1ull;
+        const int rt0 = (int)(rtot & F), rt1 = (int)((rtot >> 21) & F), rt2 = (int)(rtot >> 42);
+        const int soff[3] = {0, rt0, rt0 + rt1};
+        const uint32_t kbase = (uint32_t)(x * 32);
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            const int cnt = __popc(seg[k]);
-            int incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int n = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += n;
-            }
-            if (lane == 31) sh[k][w] = incl;
-            __syncthreads();
-            int before = 0, round_tot = 0;
-            for (int y = 0; y < kPlanThreads / 32; ++y) {
-                const int t = sh[k][y];
-                before += (y < w) ? t : 0;
-                round_tot += t;
-            }
-            int pos = before + incl - cnt;
+            // bits taken from the top, written backwards into [start, start + popc)
+            int pos = soff[k] + (int)(((excl + cnt) >> (21 * k)) & F);
             uint32_t m = seg[k];
             while (m) {
-                const int bit = __ffs(m) - 1;
-                const uint32_t mb = 1u << bit;
-                const uint32_t mem = ((bw[0] & mb) ? 1u : 0u) | ((bw[1] & mb) ? 2u : 0u) | ((bw[2] & mb) ? 4u : 0u) |
-                                     ((bw[3] & mb) ? 8u : 0u);
-                stage[pos++] = (uint32_t)(x * 32 + bit) | (mem << 28);
-                m &= m - 1;
+                const int bit = 31 - __clz(m);
+                const uint32_t mem = ((bw[0] >> bit) & 1u) | (((bw[1] >> bit) & 1u) << 1) |
+                                     (((bw[2] >> bit) & 1u) << 2) | (((bw[3] >> bit) & 1u) << 3);
+                stage[--pos] = (kbase + (uint32_t)bit) | (mem << 28);
+                m ^= 1u << bit;
             }
-            __syncthreads();
-            for (int t = tid; t < round_tot; t += kPlanThreads) wl[run[k] + t] = stage[t];
-            run[k] += round_tot;
-            __syncthreads();
         }
+        __syncthreads();
+        const int rsum = rt0 + rt1 + rt2;
+        for (int t = tid; t < rsum; t += kPlanThreads) {
+            const int64_t dst = t < rt0 ? run[0] + t : (t < rt0 + rt1 ? run[1] + (t - rt0) : run[2] + (t - rt0 - rt1));
+            wl[dst] = stage[t];
+        }
+        run[0] += rt0;
+        run[1] += rt1;
+        run[2] += rt2;
+        __syncthreads();
     }
     if (tid == 0) {
         wl_len[3 * item] = tot[0];
