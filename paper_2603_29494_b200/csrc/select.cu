@@ -330,7 +330,9 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
                         if (j >= nvis) break;
                         const uint32_t u = f32_order_key(v[j]);
                         const bool match = (pass == 0) || ((u >> (32 - 8 * pass)) == tk_prefix);
-                        if (match) hist[((u >> (24 - 8 * pass)) & 255u) * 128 + r] += 1u;
+                        // shared-memory reduction (RED, no returned value): consecutive scores in
+                        // the same bin do not serialise on a load-add-store round trip
+                        if (match) atomicAdd(&hist[((u >> (24 - 8 * pass)) & 255u) * 128 + r], 1u);
                     }
                 } else if constexpr (EPI == EPI_TOPK_EMIT) {
 #pragma unroll
