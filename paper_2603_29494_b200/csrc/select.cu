@@ -33,7 +33,13 @@ namespace va {
 
 namespace {
 
-constexpr int kThreads = 192;
+// w0 TMA producer, w1 MMA issuer, then the epilogue warps: 4 (thread = pooled row), or 8 for
+// the TOPK histogram passes, whose two warp sets take alternate 64-key chunks of every tile
+// and update the same per-row histogram with shared-memory atomics.
+template <int EPI>
+constexpr int epi_warps() { return EPI == EPI_TOPK_HIST ? 8 : 4; }
+template <int EPI>
+constexpr int sel_threads() { return 64 + 32 * epi_warps<EPI>(); }
 
 template <int D, int BN, int STAGES, int EPI>
 struct SelCfg {
@@ -56,7 +62,7 @@ VA_DEV float fmax3(float a, float b, float c) { return fmaxf(fmaxf(a, b), c); }
 }  // namespace
 
 template <int D, int BN, int STAGES, int EPI, int BK>
-__global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_constant__ SelectParams p) {
+__global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __grid_constant__ SelectParams p) {
     using C = SelCfg<D, BN, STAGES, EPI>;
     extern __shared__ __align__(1024) uint8_t smem[];
 
@@ -98,7 +104,7 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&acc_full[s], 1);
-            mbar_init(&acc_empty[s], 128);
+            mbar_init(&acc_empty[s], 32 * epi_warps<EPI>());
         }
         fence_barrier_init();
     }
@@ -156,6 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
     } else {
         // ================================================================ epilogue
         const uint32_t quad = warp & 3u;
+        const int eset = ((int)warp - 2) >> 2;     // epilogue warp set (TOPK_HIST: 2 sets)
         const int r = (int)(quad * 32 + lane);
         const int64_t i = m0 + r;                  // pooled row within head
         const bool row_ok = i < p.Np;
@@ -198,7 +205,9 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
                 }
             }
             if constexpr (EPI == EPI_TOPK_HIST) {
-                for (int bin = 0; bin < 256; ++bin) hist[bin * 128 + r] = 0u;  // own column only
+                if (eset == 0)
+                    for (int bin = 0; bin < 256; ++bin) hist[bin * 128 + r] = 0u;  // own column only
+                named_bar_sync(1, 32 * epi_warps<EPI>());                       // zeroed before any update
             }
         }
 
@@ -210,6 +219,9 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
             uint32_t words[BN / 32];
 #pragma unroll
             for (int c = 0; c < BN / 64; ++c) {
+                if constexpr (epi_warps<EPI>() == 8) {
+                    if ((c & 1) != eset) continue;  // the other warp set's 64-key chunk
+                }
                 uint32_t va_[32], vb_[32];
                 const uint32_t taddr = tmem_base + ((quad * 32u) << 16) + (uint32_t)(buf * BN + c * 64);
                 tmem_ld32(taddr, va_);
@@ -324,28 +336,48 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
                         w1 &= nvis >= 64 ? 0xffffffffu : (nvis <= 32 ? 0u : ((1u << (nvis - 32)) - 1u));
                     }
                 } else if constexpr (EPI == EPI_TOPK_HIST) {
+                    // branch-free: invisible keys are masked by a predicate, the prefix test of
+                    // passes > 0 and the histogram update are predicated shared-memory atomics
                     const int pass = p.pass;
+                    const bool all = pass == 0;
+                    const uint32_t sh_pre = (uint32_t)(32 - 8 * pass) & 31u, sh_dig = (uint32_t)(24 - 8 * pass);
+                    uint32_t* hcol = hist + r;
 #pragma unroll
                     for (int j = 0; j < 64; ++j) {
-                        if (j >= nvis) break;
                         const uint32_t u = f32_order_key(v[j]);
-                        const bool match = (pass == 0) || ((u >> (32 - 8 * pass)) == tk_prefix);
-                        // shared-memory reduction (RED, no returned value): consecutive scores in
-                        // the same bin do not serialise on a load-add-store round trip
-                        if (match) atomicAdd(&hist[((u >> (24 - 8 * pass)) & 255u) * 128 + r], 1u);
+                        const bool match = (j < nvis) && (all || (u >> sh_pre) == tk_prefix);
+                        if (match) atomicAdd(hcol + ((u >> sh_dig) & 255u) * 128, 1u);
                     }
                 } else if constexpr (EPI == EPI_TOPK_EMIT) {
+                    // keep = key above the k-th largest's key, or equal to it while ties remain
+                    // (lowest index first).  Strictly-greater and equal keys are bit-packed
+                    // branch-free; the rare ties are then taken from the lowest set bits.
+                    uint32_t e0 = 0u, e1 = 0u;
 #pragma unroll
-                    for (int j = 0; j < 64; ++j) {
-                        if (j >= nvis) break;
-                        const uint32_t u = f32_order_key(v[j]);
-                        bool keep = u > tk_prefix;
-                        if (u == tk_prefix && tk_taken < tk_krem) {
-                            keep = true;
-                            ++tk_taken;
+                    for (int j = 0; j < 32; ++j) {
+                        const uint32_t ua = f32_order_key(v[j]), ub = f32_order_key(v[32 + j]);
+                        w0 |= (ua > tk_prefix ? 1u : 0u) << j;
+                        w1 |= (ub > tk_prefix ? 1u : 0u) << j;
+                        e0 |= (ua == tk_prefix ? 1u : 0u) << j;
+                        e1 |= (ub == tk_prefix ? 1u : 0u) << j;
+                    }
+                    const uint32_t vm0 = nvis >= 32 ? 0xffffffffu : ((1u << nvis) - 1u);
+                    const uint32_t vm1 = nvis >= 64 ? 0xffffffffu : (nvis <= 32 ? 0u : ((1u << (nvis - 32)) - 1u));
+                    w0 &= vm0;
+                    w1 &= vm1;
+                    e0 &= vm0;
+                    e1 &= vm1;
+                    while ((e0 | e1) != 0u && tk_taken < tk_krem) {
+                        if (e0) {
+                            const uint32_t lo = e0 & (0u - e0);
+                            w0 |= lo;
+                            e0 ^= lo;
+                        } else {
+                            const uint32_t lo = e1 & (0u - e1);
+                            w1 |= lo;
+                            e1 ^= lo;
                         }
-                        if (j < 32) w0 |= (keep ? 1u : 0u) << j;
-                        else w1 |= (keep ? 1u : 0u) << (j - 32);
+                        ++tk_taken;
                     }
                 }
                 words[2 * c] = w0;
@@ -366,6 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
             }
         }
 
+        if constexpr (EPI == EPI_TOPK_HIST) named_bar_sync(1, 32 * epi_warps<EPI>());  // both sets' updates done
         if (row_ok) {
             if constexpr (EPI == EPI_ALG1 || EPI == EPI_THRESH || EPI == EPI_TOPK_EMIT) {
                 if (cnt) atomicAdd(&p.counts[grow], cnt);
@@ -373,6 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
                 if (p.split) p.segmax[grow * p.n_seg + seg] = f32_order_key(m_run);
                 else if (m_run > -INFINITY) atomicMax(&p.rowmax[grow], f32_order_key(m_run));
             } else if constexpr (EPI == EPI_TOPK_HIST) {
+              if (eset == 0) {
                 // find the bin holding the krem-th largest remaining key (scan from the top)
                 uint32_t cum = 0;
                 int bin = 255;
@@ -383,6 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1) select_kernel(const __grid_consta
                 }
                 p.tk_prefix[grow] = (tk_prefix << 8) | (uint32_t)bin;
                 p.tk_krem[grow] = tk_krem - cum;
+              }
             }
         }
     }
@@ -403,7 +438,7 @@ static cudaError_t launch_sel_t(const SelectParams& p, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     const int64_t units = p.BH * p.n_mt * p.n_seg;
     if (units <= 0) return cudaSuccess;
-    kern<<<(unsigned)units, kThreads, C::kSmem, st>>>(p);
+    kern<<<(unsigned)units, sel_threads<EPI>(), C::kSmem, st>>>(p);
     return cudaGetLastError();
 }
 
