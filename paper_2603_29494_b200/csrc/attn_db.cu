@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
             tma_prefetch_desc(&p.tm_v);
         }
         int qi = 0;
+        const uint64_t pol_stream = l2_evict_first_policy();  // Q is read once: do not displace K/V in L2
         for (int it = 0;; ++it) {
             const int slot = it & 1;
             int item = 0;
@@ -181,8 +182,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                 for (int t = 0; t < 2; ++t)
 #pragma unroll
                     for (int cb = 0; cb < C::kCB; ++cb)
-                        tma_load_3d(sQ + t * C::kQTileBytes + cb * 128 * 128, &p.tm_q, &bars[C::B_QFULL], cb * 64,
-                                    (int)(I.it * 256 + t * 128), (int)I.bh);
+                        tma_load_3d_hint(sQ + t * C::kQTileBytes + cb * 128 * 128, &p.tm_q, &bars[C::B_QFULL],
+                                         cb * 64, (int)(I.it * 256 + t * 128), (int)I.bh, pol_stream);
             }
             ++qi;
         }
@@ -218,8 +219,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                 ch.len = 0;
                 ch.start = 0;
                 if (j < I.n_chunks) ch = chunk_info<true>(I, j);
-                uint32_t e0 = (int)lane < ch.len ? __ldg(wlp + ch.start + lane) : 0u;
-                uint32_t e1 = 32 + (int)lane < ch.len ? __ldg(wlp + ch.start + 32 + lane) : 0u;
+                uint32_t e0 = (int)lane < ch.len ? __ldcs(wlp + ch.start + lane) : 0u;
+                uint32_t e1 = 32 + (int)lane < ch.len ? __ldcs(wlp + ch.start + 32 + lane) : 0u;
                 for (; j < I.n_chunks; j += kLoadWarps) {
                     const int64_t cc = c + j;
                     const int s = (int)(cc % S_);
@@ -228,8 +229,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                     chn.len = 0;
                     chn.start = 0;
                     if (j + kLoadWarps < I.n_chunks) chn = chunk_info<true>(I, j + kLoadWarps);
-                    const uint32_t en0 = (int)lane < chn.len ? __ldg(wlp + chn.start + lane) : 0u;
-                    const uint32_t en1 = 32 + (int)lane < chn.len ? __ldg(wlp + chn.start + 32 + lane) : 0u;
+                    const uint32_t en0 = (int)lane < chn.len ? __ldcs(wlp + chn.start + lane) : 0u;
+                    const uint32_t en1 = 32 + (int)lane < chn.len ? __ldcs(wlp + chn.start + 32 + lane) : 0u;
                     const bool ok0 = (int)lane < ch.len, ok1 = 32 + (int)lane < ch.len;
                     const uint32_t key0 = e0 & kKeyMask, key1 = e1 & kKeyMask;
                     const int r0 = (int)(bh_kv * p.N + (ok0 ? key0 : 0u));
@@ -590,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                             w.y = pack_bf16x2(__uint_as_float(ov[t + 2]) * inv, __uint_as_float(ov[t + 3]) * inv);
                             w.z = pack_bf16x2(__uint_as_float(ov[t + 4]) * inv, __uint_as_float(ov[t + 5]) * inv);
                             w.w = pack_bf16x2(__uint_as_float(ov[t + 6]) * inv, __uint_as_float(ov[t + 7]) * inv);
-                            *reinterpret_cast<uint4*>(orow + g * 32 + t) = w;
+                            __stcs(reinterpret_cast<uint4*>(orow + g * 32 + t), w);  // streamed: evict first
                         }
                     }
                 }

@@ -77,6 +77,19 @@ VA_DEV void tma_load_3d(void* dst, const void* desc, uint64_t* bar, int c0, int 
         "l"(desc), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
+// 3-D tile load with an L2 cache-policy hint (createpolicy value).
+VA_DEV void tma_load_3d_hint(void* dst, const void* desc, uint64_t* bar, int c0, int c1, int c2, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+        "l"(desc), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+        : "memory");
+}
+VA_DEV uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 // 2-D row gather: 4 rows (r0..r3) x box-width columns starting at column c0.
 VA_DEV void tma_gather4(void* dst, const void* desc, uint64_t* bar, int c0, int r0, int r1, int r2, int r3) {
     asm volatile(
