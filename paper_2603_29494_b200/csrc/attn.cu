@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             tma_prefetch_desc(&p.tm_v);
         }
         int qi = 0;
+        const uint64_t pol_stream = l2_evict_first_policy();  // Q is read once: do not displace K/V in L2
         for (int it = 0;; ++it) {
             const int slot = it & 1;
             int item = 0;
@@ -191,8 +192,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                 for (int t = 0; t < 2; ++t)
 #pragma unroll
                     for (int cb = 0; cb < C::kCB; ++cb)
-                        tma_load_3d(sQ + t * C::kQTileBytes + cb * 128 * 128, &p.tm_q, &bars[C::B_QFULL], cb * 64,
-                                    (int)(I.it * 256 + t * 128), (int)I.bh);
+                        tma_load_3d_hint(sQ + t * C::kQTileBytes + cb * 128 * 128, &p.tm_q, &bars[C::B_QFULL], cb * 64,
+                                         (int)(I.it * 256 + t * 128), (int)I.bh, pol_stream);
             }
             ++qi;
         }
@@ -225,8 +226,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                 ch.len = 0;
                 ch.start = 0;
                 if (j < I.n_chunks) ch = chunk_info<true>(I, j);
-                uint32_t e0 = kb + (int)lane < ch.len ? __ldg(wlp + ch.start + kb + lane) : 0u;
-                uint32_t e1 = kb + 32 + (int)lane < ch.len ? __ldg(wlp + ch.start + kb + 32 + lane) : 0u;
+                uint32_t e0 = kb + (int)lane < ch.len ? __ldcs(wlp + ch.start + kb + lane) : 0u;
+                uint32_t e1 = kb + 32 + (int)lane < ch.len ? __ldcs(wlp + ch.start + kb + 32 + lane) : 0u;
                 for (; j < I.n_chunks; j += S_) {
                     const int64_t cc = c + j;
                     const int s = (int)(cc % S_);
@@ -235,8 +236,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     chn.len = 0;
                     chn.start = 0;
                     if (j + S_ < I.n_chunks) chn = chunk_info<true>(I, j + S_);
-                    const uint32_t en0 = kb + (int)lane < chn.len ? __ldg(wlp + chn.start + kb + lane) : 0u;
-                    const uint32_t en1 = kb + 32 + (int)lane < chn.len ? __ldg(wlp + chn.start + kb + 32 + lane) : 0u;
+                    const uint32_t en0 = kb + (int)lane < chn.len ? __ldcs(wlp + chn.start + kb + lane) : 0u;
+                    const uint32_t en1 = kb + 32 + (int)lane < chn.len ? __ldcs(wlp + chn.start + kb + 32 + lane) : 0u;
                     const bool ok0 = kb + (int)lane < ch.len, ok1 = kb + 32 + (int)lane < ch.len;
                     const uint32_t key0 = e0 & kKeyMask, key1 = e1 & kKeyMask;
                     const int r0 = (int)(bh_kv * p.N + (ok0 ? key0 : 0u));
@@ -590,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                             w4.y = pack_bf16x2(__uint_as_float(ov[t + 2]) * inv, __uint_as_float(ov[t + 3]) * inv);
                             w4.z = pack_bf16x2(__uint_as_float(ov[t + 4]) * inv, __uint_as_float(ov[t + 5]) * inv);
                             w4.w = pack_bf16x2(__uint_as_float(ov[t + 6]) * inv, __uint_as_float(ov[t + 7]) * inv);
-                            *reinterpret_cast<uint4*>(orow + gq * 32 + t) = w4;
+                            __stcs(reinterpret_cast<uint4*>(orow + gq * 32 + t), w4);  // streamed: evict first
                         }
                     }
                 }
