@@ -229,6 +229,24 @@ def build_inputs(wl, kind, dev, h0, h1):
     return q, k, v
 
 # ---------------------------------------------------------------------------- ours
+def e2e_groups(n):
+    """KV-head group sizes for the pipelined end-to-end step: 1, 2, 4, 7, ... (x1.6, at most 8)
+    then a 2, 1 tail.  The first group's H2D and the last group's D2H are the only copies not
+    overlapped with compute; the growth keeps each group's H2D close to the previous group's
+    compute time (about 1.8 ms of PCIe per 3.3 ms of compute per head at dit128k)."""
+    if n <= 3:
+        return [1] * n
+    tail = [2, 1] if n >= 8 else [1]
+    body = n - sum(tail)
+    sizes, step = [], 1
+    while body > 0:
+        t = min(step, body)
+        sizes.append(t)
+        body -= t
+        step = min(int(step * 1.6) + 1, 8)
+    return sizes + tail
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -426,14 +444,18 @@ def run_ours(args):
         vh.copy_(v)
         qd, kd, vd = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
 
-        # Host copies overlap the compute: the local heads run as up to 4 KV-head groups;
-        # group g's H2D (copy stream) runs while group g-1 computes, and (one rank) group
-        # g-1's output D2H (second copy stream) while group g computes.
+        # Host copies overlap the compute: the local heads run as KV-head groups; group g's
+        # H2D (copy stream) runs while group g-1 computes, and (one rank) group g-1's output
+        # D2H (second copy stream) while group g computes.  Group sizes ramp up from one KV
+        # head and back down (e2e_groups), so only one head's H2D and one head's D2H are not
+        # hidden behind compute.
         nkv, nq = k.shape[1], q.shape[1]
         rep_l = nq // nkv
-        n_ch = min(4, nkv) if B == 1 else 1
-        cb = [round(i * nkv / n_ch) for i in range(n_ch + 1)]
-        chunks = [(cb[i] * rep_l, cb[i + 1] * rep_l, cb[i], cb[i + 1]) for i in range(n_ch)]
+        sizes = e2e_groups(nkv) if B == 1 else [nkv]
+        cb = [0]
+        for g in sizes:
+            cb.append(cb[-1] + g)
+        chunks = [(cb[i] * rep_l, cb[i + 1] * rep_l, cb[i], cb[i + 1]) for i in range(len(sizes))]
         s_h2d, s_d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
 
         def e2e_step():

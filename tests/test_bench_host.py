@@ -29,3 +29,14 @@ def test_build_inputs_gqa_mapping_for_unaligned_ranges():
                 g = (h0 + i) // 7
                 assert torch.equal(k[:, i // (nq // nkv)], full_k[:, g])
                 assert torch.equal(v[:, i // (nq // nkv)], full_v[:, g])
+
+
+def test_e2e_groups_cover_all_kv_heads_with_small_ends():
+    """The pipelined e2e step's KV-head groups partition the heads and start and end with a
+    single head, so only one head's H2D and one head's D2H are exposed (bench.e2e_groups)."""
+    import bench
+    for n in range(1, 65):
+        g = bench.e2e_groups(n)
+        assert sum(g) == n and min(g) >= 1
+        assert g[0] == 1 and g[-1] == 1
+        assert max(g) <= 8
