@@ -457,25 +457,35 @@ def run_ours(args):
             cb.append(cb[-1] + g)
         chunks = [(cb[i] * rep_l, cb[i + 1] * rep_l, cb[i], cb[i + 1]) for i in range(len(sizes))]
         s_h2d, s_d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        # Consecutive groups alternate between two compute streams with their own selection
+        # and plan buffers, so one group's attention tail overlaps the next group's start.
+        stream2 = torch.cuda.Stream(device=dev)
+        sets = [(stream, offsets, indices, d_nnz, ws_fwd),
+                (stream2, torch.empty_like(offsets), torch.empty_like(indices), torch.empty_like(d_nnz),
+                 torch.empty_like(ws_fwd))]
 
         def e2e_step():
             s_h2d.wait_stream(stream)
-            for (q0, q1, k0, k1) in chunks:
+            stream2.wait_stream(stream)
+            for gi, (q0, q1, k0, k1) in enumerate(chunks):
+                st_c, off_c, idx_c, nnz_c, ws_c = sets[gi % 2]
                 with torch.cuda.stream(s_h2d):
                     qd[:, q0:q1].copy_(qh[:, q0:q1], non_blocking=True)
                     kd[:, k0:k1].copy_(kh[:, k0:k1], non_blocking=True)
                     vd[:, k0:k1].copy_(vh[:, k0:k1], non_blocking=True)
                     ev_in = torch.cuda.Event()
                     ev_in.record(s_h2d)
-                stream.wait_event(ev_in)
-                va.forward_into(qd[:, q0:q1], kd[:, k0:k1], vd[:, k0:k1], cfg, offsets, indices, cap, d_nnz, cap,
-                                o[:, q0:q1], lse[:, q0:q1], ws_fwd, causal)
+                st_c.wait_event(ev_in)
+                with torch.cuda.stream(st_c):
+                    va.forward_into(qd[:, q0:q1], kd[:, k0:k1], vd[:, k0:k1], cfg, off_c, idx_c, cap, nnz_c, cap,
+                                    o[:, q0:q1], lse[:, q0:q1], ws_c, causal)
+                ev_out = torch.cuda.Event()
+                ev_out.record(st_c)
                 if ws == 1:
-                    ev_out = torch.cuda.Event()
-                    ev_out.record(stream)
                     with torch.cuda.stream(s_d2h):
                         s_d2h.wait_event(ev_out)
                         oh_host[:, q0:q1].copy_(o[:, q0:q1], non_blocking=True)
+            stream.wait_stream(stream2)
             if ws > 1:
                 allgather_heads(o, o_pad, o_all)
                 oh_host.copy_(o_all, non_blocking=True)
