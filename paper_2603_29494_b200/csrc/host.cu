@@ -110,6 +110,7 @@ struct SelectWs {
     uint32_t* segmax;
     uint32_t* tk_prefix;
     uint32_t* tk_krem;
+    uint32_t* tk_hist;
     size_t total;
 };
 
@@ -132,6 +133,8 @@ SelectWs carve_select(const vecattn_problem_t* p, int32_t pq, void* base) {
     off += align_up((size_t)R * 4);
     w.tk_krem = reinterpret_cast<uint32_t*>(b + off);
     off += align_up((size_t)R * 4);
+    w.tk_hist = reinterpret_cast<uint32_t*>(b + off);
+    off += align_up((size_t)R * 256 * 4);
     w.total = off;
     return w;
 }
@@ -170,8 +173,8 @@ void plan_segments(const vecattn_problem_t* p, const vecattn_select_params_t* s,
             const int64_t L = G / gcd64(G, 256) * 256;
             if (L < p->N) seg = L * std::max<int64_t>(1, 16384 / L);
         }
-    } else if (epi == va::EPI_MAX || epi == va::EPI_THRESH || epi == va::EPI_SCORES) {
-        seg = 16384;
+    } else if (epi == va::EPI_MAX || epi == va::EPI_THRESH || epi == va::EPI_SCORES || epi == va::EPI_TOPK_HIST) {
+        seg = 16384;  // TOPK histogram passes: per-segment histograms are summed in tk_hist
     }
     if (seg > Nr) seg = Nr;
     // few rows (e.g. one GPU's share of the heads): shorter segments until the units fill
@@ -210,6 +213,7 @@ vecattn_status_t fill_select_params(const vecattn_problem_t* p, const vecattn_se
     sp.segmax = w.segmax;
     sp.tk_prefix = w.tk_prefix;
     sp.tk_krem = w.tk_krem;
+    sp.tk_hist = w.tk_hist;
     sp.topk = s ? s->topk : 0;
     sp.keep_frac = s ? s->keep_frac : 0.f;
     const float scale = eff_scale(p);
@@ -265,7 +269,11 @@ cudaError_t run_select(const vecattn_problem_t* p, const vecattn_select_params_t
             if (e == cudaSuccess) e = run(va::EPI_MAX, 0);
             if (e == cudaSuccess) e = run(va::EPI_THRESH, 0);
         } else {
-            for (int pass = 0; pass < 4 && e == cudaSuccess; ++pass) e = run(va::EPI_TOPK_HIST, pass);
+            for (int pass = 0; pass < 4 && e == cudaSuccess; ++pass) {
+                e = cudaMemsetAsync(w.tk_hist, 0, (size_t)R * 256 * 4, cs);
+                if (e == cudaSuccess) e = run(va::EPI_TOPK_HIST, pass);
+                if (e == cudaSuccess) e = va::launch_topk_pick(sp, cs);
+            }
             if (e == cudaSuccess) e = run(va::EPI_TOPK_EMIT, 0);
         }
     }

@@ -43,6 +43,7 @@ struct SelectParams {
                                    // each segment's running max at the max of the earlier segments
     uint32_t* tk_prefix;           // [BH*Np] TOPK radix state
     uint32_t* tk_krem;             // [BH*Np]
+    uint32_t* tk_hist;             // [BH*Np][256] TOPK radix histogram of the pass (summed over key segments)
     float* scores_out;             // EPI_SCORES: [BH*Np, N] fp32 (debug)
     int32_t pass;                  // TOPK pass 0..3
     int64_t topk;                  // TOPK budget
@@ -51,6 +52,9 @@ struct SelectParams {
 };
 
 cudaError_t launch_select(const SelectParams& p, int epi, int D, cudaStream_t st);
+// TOPK: after a histogram pass, per row: the digit bin holding the k_rem-th largest remaining
+// key -> tk_prefix <<= 8 | bin, tk_krem -= keys in higher bins.
+cudaError_t launch_topk_pick(const SelectParams& p, cudaStream_t st);
 
 // ---------------------------------------------------------------------- compaction
 // offsets[r+1] = sum counts[0..r]; d_nnz = total.

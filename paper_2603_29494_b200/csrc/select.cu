@@ -406,18 +406,13 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
                 if (p.split) p.segmax[grow * p.n_seg + seg] = f32_order_key(m_run);
                 else if (m_run > -INFINITY) atomicMax(&p.rowmax[grow], f32_order_key(m_run));
             } else if constexpr (EPI == EPI_TOPK_HIST) {
-              if (eset == 0) {
-                // find the bin holding the krem-th largest remaining key (scan from the top)
-                uint32_t cum = 0;
-                int bin = 255;
-                for (; bin > 0; --bin) {
+                // this key segment's counts -> the row's histogram in global memory (the two
+                // warp sets flush half of the bins each; most bins are empty)
+                uint32_t* gh = p.tk_hist + grow * 256;
+                for (int bin = 128 * eset; bin < 128 * eset + 128; ++bin) {
                     const uint32_t hc = hist[bin * 128 + r];
-                    if (cum + hc >= tk_krem) break;
-                    cum += hc;
+                    if (hc) atomicAdd(gh + bin, hc);
                 }
-                p.tk_prefix[grow] = (tk_prefix << 8) | (uint32_t)bin;
-                p.tk_krem[grow] = tk_krem - cum;
-              }
             }
         }
     }
@@ -428,6 +423,39 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
         tc_fence_after();
         tmem_dealloc<C::kTmemCols>(tmem_base);
     }
+}
+
+// TOPK: one thread per pooled row after each histogram pass (see launch_topk_pick).
+__global__ void __launch_bounds__(256) topk_pick_kernel(const __grid_constant__ SelectParams p) {
+    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= p.BH * p.Np) return;
+    const int64_t i = row % p.Np;
+    const int64_t vis_end = p.causal ? min(p.N, (i + 1) * (int64_t)p.pq) : p.N;
+    uint32_t prefix, krem;
+    if (p.pass == 0) {  // k_i = min(topk, visible), or round_half_up(keep_frac * visible) in [1, visible]
+        int64_t ki;
+        if (p.topk > 0) ki = min(p.topk, vis_end);
+        else {
+            ki = (int64_t)floor((double)p.keep_frac * (double)vis_end + 0.5);
+            ki = max((int64_t)1, min(ki, vis_end));
+        }
+        prefix = 0;
+        krem = (uint32_t)ki;
+    } else {
+        prefix = p.tk_prefix[row];
+        krem = p.tk_krem[row];
+    }
+    // the bin holding the krem-th largest remaining key (scan from the top)
+    const uint32_t* h = p.tk_hist + row * 256;
+    uint32_t cum = 0;
+    int bin = 255;
+    for (; bin > 0; --bin) {
+        const uint32_t hc = h[bin];
+        if (cum + hc >= krem) break;
+        cum += hc;
+    }
+    p.tk_prefix[row] = (prefix << 8) | (uint32_t)bin;
+    p.tk_krem[row] = krem - cum;
 }
 
 template <int D, int BN, int STAGES, int EPI, int BK = 16>
@@ -465,6 +493,13 @@ cudaError_t launch_select(const SelectParams& p, int epi, int D, cudaStream_t st
     if (D == 128) return launch_sel_d<128>(p, epi, st);
     if (D == 64) return launch_sel_d<64>(p, epi, st);
     return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_topk_pick(const SelectParams& p, cudaStream_t st) {
+    const int64_t R = p.BH * p.Np;
+    if (R <= 0) return cudaSuccess;
+    topk_pick_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(p);
+    return cudaGetLastError();
 }
 
 }  // namespace va
