@@ -84,6 +84,9 @@ SEL_CASES = [
     ("gauss", 1, 1, 1, 2048, 64, 64, False, "topk", 16, 16, 0.0, 100, 0.0),
     ("video", 1, 2, 1, 4096, 128, 64, False, "alg1", 32, 4, 1.0, 0, 0.0),
     ("video", 1, 2, 1, 4096, 128, 64, True, "alg1", 64, 3, 1.0, 0, 0.0),
+    # TOPK rows longer than one 16K-key histogram segment: per-segment histograms are summed
+    ("video", 1, 1, 1, 40000 + 37, 128, 64, True, "topk", 16, 16, 0.0, 0, 0.2),
+    ("gauss", 1, 1, 1, 33000, 128, 64, False, "topk", 16, 16, 0.0, 500, 0.0),
 ]
 
 
