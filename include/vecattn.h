@@ -129,7 +129,12 @@ VECATTN_API size_t vecattn_forward_workspace_bytes(const vecattn_problem_t* p, c
  * selection bitmask.  `offsets` and `*d_nnz` are always written; `indices` (CSR, may
  * be NULL with cap = 0) is written iff nnz <= cap.  The attention runs iff
  * nnz <= nnz_cap (the workspace's plan capacity); otherwise o/lse are untouched and the
- * caller reads d_nnz, grows the workspace and calls again.                          */
+ * caller reads d_nnz, grows the workspace and calls again.
+ * Streams: for non-causal problems the CSR emission runs on a library-owned side stream
+ * beside the attention kernel.  It is forked from `stream` with an event after the plan
+ * and joined back into `stream` with an event before the call's work ends. Every output is
+ * therefore complete when `stream` reaches that point, and the fork/join can be captured
+ * in a CUDA graph. Setting VECATTN_SERIAL_EMIT=1 emits on `stream` instead.       */
 VECATTN_API vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_select_params_t* s,
                                              const void* q, const void* k, const void* v, int64_t* offsets,
                                              int32_t* indices, int64_t cap, int64_t* d_nnz, int64_t nnz_cap,

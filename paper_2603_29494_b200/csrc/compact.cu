@@ -9,6 +9,8 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <algorithm>
+
 namespace va {
 
 // Single-CTA exclusive scan over R row counts (R = B*Hq*N_p, <= a few 1e5).
@@ -53,6 +55,7 @@ __global__ void __launch_bounds__(1024) scan_kernel(const unsigned long long* __
 // so the index stores are coalesced.
 constexpr int kEmitWarps = 8;
 
+template <int kEmitWarps, bool STREAM>
 __global__ void __launch_bounds__(kEmitWarps * 32) emit_kernel(const uint32_t* __restrict__ bitmask,
                                                                  int64_t words_per_row,
                                                                  const int64_t* __restrict__ offsets,
@@ -70,10 +73,11 @@ __global__ void __launch_bounds__(kEmitWarps * 32) emit_kernel(const uint32_t* _
         const int64_t nwords = (vis + 31) / 32;
         const uint32_t* src = bitmask + row * words_per_row;
         int64_t out = offsets[row];
-        uint32_t next = lane < nwords ? __ldg(src + lane) : 0u;  // software-pipelined by one round
+        auto ld = [&](const uint32_t* a) { return STREAM ? __ldcs(a) : __ldg(a); };
+        uint32_t next = lane < nwords ? ld(src + lane) : 0u;  // software-pipelined by one round
         for (int64_t w0 = 0; w0 < nwords; w0 += 32) {
             uint32_t word = next;
-            next = (w0 + 32 + lane < nwords) ? __ldg(src + w0 + 32 + lane) : 0u;
+            next = (w0 + 32 + lane < nwords) ? ld(src + w0 + 32 + lane) : 0u;
             const int pc = __popc(word);
             int incl = pc;
 #pragma unroll
@@ -90,7 +94,10 @@ __global__ void __launch_bounds__(kEmitWarps * 32) emit_kernel(const uint32_t* _
                 word ^= 1u << bit;
             }
             __syncwarp();
-            for (int t = lane; t < total; t += 32) indices[out + t] = stage[w][t];
+            for (int t = lane; t < total; t += 32) {
+                if constexpr (STREAM) __stcs(indices + out + t, stage[w][t]);
+                else indices[out + t] = stage[w][t];
+            }
             __syncwarp();
             out += total;
         }
@@ -110,8 +117,20 @@ cudaError_t launch_emit(const uint32_t* bitmask, int64_t words_per_row, const in
     int64_t blocks = (R + kEmitWarps - 1) / kEmitWarps;
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
-    emit_kernel<<<(unsigned)blocks, kEmitWarps * 32, 0, st>>>(bitmask, words_per_row, offsets, d_nnz, cap, indices,
-                                                              BH, Np, N, pq, causal);
+    emit_kernel<kEmitWarps, false><<<(unsigned)blocks, kEmitWarps * 32, 0, st>>>(
+        bitmask, words_per_row, offsets, d_nnz, cap, indices, BH, Np, N, pq, causal);
+    return cudaGetLastError();
+}
+
+// Emission beside the attention kernel (vecattn_forward): one 2-warp CTA per SM, 8 KB of
+// shared memory, so it fits next to the persistent attention CTA and runs on that SM's
+// spare issue slots; bitmask reads and index stores are streamed (evict-first) so they do
+// not displace the K/V rows the attention gathers from L2.
+cudaError_t launch_emit_shadow(const uint32_t* bitmask, int64_t words_per_row, const int64_t* offsets,
+                               const int64_t* d_nnz, int64_t cap, int32_t* indices, int64_t BH, int64_t Np,
+                               int64_t N, int32_t pq, int32_t causal, int sms, cudaStream_t st) {
+    emit_kernel<2, true><<<(unsigned)std::max(1, sms), 64, 0, st>>>(bitmask, words_per_row, offsets, d_nnz, cap,
+                                                                    indices, BH, Np, N, pq, causal);
     return cudaGetLastError();
 }
 

@@ -306,6 +306,33 @@ __global__ void validate_kernel(const int64_t* __restrict__ offsets, const int32
 
 }  // namespace
 
+namespace {
+// Library-owned side stream per device for the emission that runs beside the attention
+// kernel, with its fork/join events.  Created once; the mutex serialises the
+// record -> wait -> launch -> record -> wait sequence of concurrent host callers.
+struct SideStream {
+    std::mutex mu;
+    cudaStream_t s = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int sms = va::kNumSMsB200;
+};
+SideStream g_side[64];
+std::mutex g_side_init;
+SideStream* side_stream() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> g(g_side_init);
+    SideStream& x = g_side[dev];
+    if (!x.s) {
+        if (cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        cudaEventCreateWithFlags(&x.ev_fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&x.ev_join, cudaEventDisableTiming);
+        cudaDeviceGetAttribute(&x.sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return &x;
+}
+}  // namespace
+
 extern "C" {
 
 int32_t vecattn_abi_version(void) { return 1; }
@@ -760,10 +787,18 @@ vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_selec
     ap->d_nnz = d_nnz;
     ap->nnz_cap = nnz_cap;
     if (g_timing.enabled) tbegin(true, true);
+    // The CSR (the caller's index lists) is not an input of the attention, which reads the
+    // plan: by default it is emitted on a side stream beside the attention kernel (one small
+    // CTA per SM next to the persistent attention CTA), forked after the plan and joined
+    // before the call's work on `stream` ends.  VECATTN_SERIAL_EMIT=1 emits before the plan.
+    const bool emit = indices && cap > 0;
+    // (non-causal only: the causal attention kernel holds all 64K registers of its SM, so a
+    // side CTA could not run beside it)
+    SideStream* side = (emit && !p->causal && !getenv("VECATTN_SERIAL_EMIT")) ? side_stream() : nullptr;
     tmark(0, cs);
     cudaError_t e = run_select(p, s, q, k, offsets, d_nnz, w, *sp, cs);
     tmark(1, cs);
-    if (e == cudaSuccess && indices && cap > 0)
+    if (e == cudaSuccess && emit && !side)
         e = va::launch_emit(w.bitmask, sp->words_per_row, offsets, d_nnz, cap, indices, sp->BH, sp->Np, p->N, s->pq,
                             p->causal ? 1 : 0, cs);
     if (e == cudaSuccess)
@@ -771,8 +806,21 @@ vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_selec
                             s->pq, p->causal ? 1 : 0, cs);
     if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, sizeof(int), cs);
     tmark(2, cs);
+    std::unique_lock<std::mutex> lk;
+    if (e == cudaSuccess && side) {
+        lk = std::unique_lock<std::mutex>(side->mu);
+        e = cudaEventRecord(side->ev_fork, cs);
+    }
     if (e == cudaSuccess) e = va::launch_attn(*ap, (int)p->D, true, attn_grid(ap->total_items), cs);
     tmark(3, cs);
+    if (e == cudaSuccess && side) {
+        e = cudaStreamWaitEvent(side->s, side->ev_fork, 0);
+        if (e == cudaSuccess)
+            e = va::launch_emit_shadow(w.bitmask, sp->words_per_row, offsets, d_nnz, cap, indices, sp->BH, sp->Np,
+                                       p->N, s->pq, p->causal ? 1 : 0, side->sms, side->s);
+        if (e == cudaSuccess) e = cudaEventRecord(side->ev_join, side->s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, side->ev_join, 0);
+    }
     delete sp;
     delete ap;
     return cuda_status(e);

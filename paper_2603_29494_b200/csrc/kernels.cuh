@@ -60,6 +60,10 @@ cudaError_t launch_topk_pick(const SelectParams& p, cudaStream_t st);
 // offsets[r+1] = sum counts[0..r]; d_nnz = total.
 cudaError_t launch_scan(const unsigned long long* counts, int64_t R, int64_t* offsets, int64_t* d_nnz,
                         cudaStream_t st);
+// Emission on a side stream beside the attention kernel (one small CTA per SM).
+cudaError_t launch_emit_shadow(const uint32_t* bitmask, int64_t words_per_row, const int64_t* offsets,
+                               const int64_t* d_nnz, int64_t cap, int32_t* indices, int64_t BH, int64_t Np,
+                               int64_t N, int32_t pq, int32_t causal, int sms, cudaStream_t st);
 // Emits ascending indices of set bits of each row if *d_nnz <= cap.
 cudaError_t launch_emit(const uint32_t* bitmask, int64_t words_per_row, const int64_t* offsets,
                         const int64_t* d_nnz, int64_t cap, int32_t* indices, int64_t BH, int64_t Np,
