@@ -18,6 +18,6 @@ for d in rows:
                f"{c['rho_achieved']:.3f} | {d['forward_ms']:.2f} | {st.get('select', -1):.2f} | {st.get('emit_plan', -1):.2f} | "
                f"{st.get('attention', -1):.2f} | {(d['dense_ms'] or float('nan')):.1f} | {(d['speedup_vs_dense'] or float('nan')):.2f} | "
                f"{d['roofline']['achieved']:.0f} ({d['roofline']['frac']:.2f}) | {(d['dense_tflops'] or float('nan')):.0f} | "
-               f"{sr.get('achieved', 0):.0f} | {d['clocks']['sm_mhz']:.0f} |")
+               f"{sr.get('achieved', 0):.0f} | {(d['clocks']['sm_mhz'] or float('nan')):.0f} |")
 open(os.path.join(ROOT, "profiles", f"sweep_{tag}.md"), "w").write("\n".join(out) + "\n")
 print("\n".join(out))
