@@ -1,8 +1,9 @@
 """GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
 
 Inputs are built by bench.build_inputs on the bench's workloads with bench's alpha. The
-workloads are dit128k (N = 131072, 24 heads, non-causal, the headline) and vlm128k
-(N = 131072, 28/4 heads, causal). One fused vecattn_forward produces the outputs, and the
+workloads are dit128k (N = 131072, 24 heads, non-causal, the headline), vlm128k
+(N = 131072, 28/4 heads, causal) and hy (N = 118800, 24 heads, non-causal; the last query
+block and key tile are ragged). One fused vecattn_forward produces the outputs, and the
 dense kernel is checked too.
 
 The oracle computes sampled outputs one at a time:
@@ -23,7 +24,8 @@ from tests.parity import ATOL_MAX, ATOL_MEAN, LSE_ATOL, bf16_np, compare_selecti
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("wl_name,alpha", [("dit128k", 1.0039), ("vlm128k", None)])
+@pytest.mark.parametrize("wl_name,alpha", [("dit128k", 1.0039), ("vlm128k", None),
+                                            ("hy", 1.0020)])  # HY: N = 118800, a 16-row last block
 def test_full_size_forward_sampled(wl_name, alpha):
     import bench
     import paper_2603_29494_b200.vecattn as va
