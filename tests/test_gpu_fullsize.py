@@ -3,7 +3,7 @@
 Inputs are built by bench.build_inputs on the bench's workloads with bench's alpha. The
 workloads are dit128k (N = 131072, 24 heads, non-causal, the headline), vlm128k
 (N = 131072, 28/4 heads, causal) and hy (N = 118800, 24 heads, non-causal; the last query
-block and key tile are ragged). One fused vecattn_forward produces the outputs, and the
+block and key tile are ragged) and wan (N = 75600, 40 heads, ρ ≈ 0.52). One fused vecattn_forward produces the outputs, and the
 dense kernel is checked too.
 
 The oracle computes sampled outputs one at a time:
@@ -25,7 +25,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("wl_name,alpha", [("dit128k", 1.0039), ("vlm128k", None),
-                                            ("hy", 1.0020)])  # HY: N = 118800, a 16-row last block
+                                            ("hy", 1.0020),   # HY: N = 118800, a 16-row last block
+                                            ("wan", 1.2070)])  # WAN: 40 heads, N = 75600, rho ~ 0.52
 def test_full_size_forward_sampled(wl_name, alpha):
     import bench
     import paper_2603_29494_b200.vecattn as va
