@@ -11,7 +11,7 @@ for v in A B; do
 done
 for i in $(seq $n); do for v in A B; do
   cp gpurun_out/ab/lib_$v.so paper_2603_29494_b200/libvecattn.so
-  timeout -s KILL 300 python bench.py --no-e2e --no-cpu-baseline ${ALPHA_ARGS:---alpha 1.0039} --dense-reps 0 ${BENCH_ARGS} > gpurun_out/ab/b.json 2>/dev/null
+  timeout -s KILL 300 python bench.py --no-e2e --no-cpu-baseline ${ALPHA_ARGS:---alpha 1.0039} --dense-reps 0 ${BENCH_ARGS} > gpurun_out/ab/b.json 2>gpurun_out/ab/b_$v.err
   python -c "
-import json; d=json.loads(open('gpurun_out/ab/b.json').read().strip().splitlines()[-1]); print('$v', d['stage_ms'].get('attention'), d['forward_ms'], d['clocks']['sm_mhz'])"
+import json; d=json.loads(open('gpurun_out/ab/b.json').read().strip().splitlines()[-1]); print('$v', d['stage_ms'].get('attention'), d['forward_ms'], d['clocks']['sm_mhz'])" || tail -3 gpurun_out/ab/b_$v.err
 done; done
