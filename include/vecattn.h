@@ -109,7 +109,9 @@ VECATTN_API size_t vecattn_sparse_workspace_bytes(const vecattn_problem_t* p, in
  * block i, O[rows of i] = softmax(scale * Q[rows] K[Idx(i)]^T) V[Idx(i)], causal rows
  * additionally masked to keys j <= r.  A row with no visible selected key outputs
  * O_r = V_r and LSE_r = scale*<q_r,k_r> (reading R6).  offsets/indices: CSR as
- * produced by vecattn_select (same pq); nnz = offsets[last] must be <= nnz_cap.
+ * produced by vecattn_select (same pq); nnz = offsets[last] must be <= nnz_cap (the
+ * workspace's plan capacity): if it is larger, the device skips the plan and the attention
+ * (o/lse untouched) instead of writing past the workspace.
  * Index content is NOT validated (O(nnz)); out-of-range indices are undefined
  * behaviour -- see vecattn_validate_selection.  lse may be NULL.                    */
 VECATTN_API vecattn_status_t vecattn_sparse_fwd(const vecattn_problem_t* p, int32_t pq, const void* q, const void* k,
@@ -133,8 +135,10 @@ VECATTN_API size_t vecattn_forward_workspace_bytes(const vecattn_problem_t* p, c
  * Streams: for non-causal problems the CSR emission runs on a library-owned side stream
  * beside the attention kernel.  It is forked from `stream` with an event after the plan
  * and joined back into `stream` with an event before the call's work ends. Every output is
- * therefore complete when `stream` reaches that point, and the fork/join can be captured
- * in a CUDA graph. Setting VECATTN_SERIAL_EMIT=1 emits on `stream` instead.       */
+ * therefore complete when `stream` reaches that point.  The side stream is one per device,
+ * shared by all callers (host calls serialise on it).  While `stream` is being captured into
+ * a CUDA graph the emission stays on `stream`, so a capture never includes the shared side
+ * stream.  Setting VECATTN_SERIAL_EMIT=1 emits on `stream` always.                */
 VECATTN_API vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_select_params_t* s,
                                              const void* q, const void* k, const void* v, int64_t* offsets,
                                              int32_t* indices, int64_t cap, int64_t* d_nnz, int64_t nnz_cap,

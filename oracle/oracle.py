@@ -251,10 +251,18 @@ def dense_attn(q, k, v, *, causal: bool = False, scale: float | None = None, row
     return o, lse
 
 
-def sparsity(offsets, N: int, pq: int, causal: bool) -> float:
-    """rho = 1 - sum_i C_i*h_i / S_tot, for ONE head's CSR."""
-    counts = np.diff(np.asarray(offsets, np.int64))
-    Np = counts.size
-    h = np.array([min(N, (i + 1) * pq) - i * pq for i in range(Np)], np.float64)
-    tot = N * N if not causal else N * (N + 1) / 2
-    return 1.0 - float(np.sum(counts * h)) / tot
+def sparsity(offsets, indices, N: int, pq: int, causal: bool) -> float:
+    """rho = 1 - sum_r |J_r| / S_tot (P:41 "how many entries are dropped"; S:230), DESIGN.md
+    reading R15, for ONE head's CSR: J_r is the row's visible selected keys, Idx(i) for
+    non-causal and {j in Idx(i) : j <= r} for causal (Eq. 5's mask); S_tot = N^2 or
+    N(N+1)/2 (the visible entries of the dense map).  Plain loops over blocks and rows."""
+    offsets = np.asarray(offsets, np.int64)
+    indices = np.asarray(indices, np.int64)
+    Np = offsets.size - 1
+    kept = 0
+    for i in range(Np):
+        idx = indices[offsets[i]:offsets[i + 1]]
+        for r in range(i * pq, min(N, (i + 1) * pq)):
+            kept += int(np.count_nonzero(idx <= r)) if causal else idx.size
+    tot = N * N if not causal else N * (N + 1) // 2
+    return 1.0 - kept / tot

@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             }
             // ---------------------------------------------------------------- epilogue
             // rows that only ever saw masked keys: l = 0 (non-members -> -2^100 -> 0), degenerate
-            const float l = (m_ref < -1e28f) ? 0.f : lsum2.x + lsum2.y;
+            const float l = (m_ref < -0x1p99f * sl2) ? 0.f : lsum2.x + lsum2.y;  // scale-aware: masked = -2^100*sl2
             const float inv = l > 0.f ? 1.f / l : 0.f;
             __nv_bfloat16* orow = p.o + (I.bh * p.N + qrow) * D;
             if (I.n_chunks > 0) {  // every MMA of the item complete (one OFIN phase per item with chunks)
@@ -694,10 +694,14 @@ __global__ void __launch_bounds__(kWlThreads) worklist_kernel(const int64_t* __r
                                                               const int32_t* __restrict__ indices,
                                                               uint32_t* __restrict__ wl, int32_t* __restrict__ wl_len,
                                                               int64_t BH, int64_t Np, int64_t n_it, int64_t N,
-                                                              int32_t pq, int32_t stripe_words) {
+                                                              int32_t pq, int32_t stripe_words, int64_t cap) {
     extern __shared__ uint32_t bm[];  // [4][stripe_words]
     __shared__ int sh[48];
     const int64_t item = blockIdx.x;
+    if (offsets[BH * Np] > cap) {  // plan capacity (the CSR's nnz) exceeded: no writes
+        if (threadIdx.x == 0) wl_len[3 * item] = wl_len[3 * item + 1] = wl_len[3 * item + 2] = 0;
+        return;
+    }
     const int64_t bh = item / n_it, it = item % n_it;
     const int G = 256 / pq;
     const int64_t i0 = it * G;
@@ -804,7 +808,8 @@ __global__ void __launch_bounds__(kWlThreads) worklist_kernel(const int64_t* __r
 }
 
 cudaError_t launch_worklist(const int64_t* offsets, const int32_t* indices, uint32_t* wl, int32_t* wl_len,
-                            int64_t BH, int64_t Np, int64_t n_it, int64_t N, int32_t pq, cudaStream_t st) {
+                            int64_t BH, int64_t Np, int64_t n_it, int64_t N, int32_t pq, int64_t cap,
+                            cudaStream_t st) {
     const int64_t items = BH * n_it;
     if (items <= 0) return cudaSuccess;
     const int stripe_words = (int)min((int64_t)kStripeWords, (N + 31) / 32);
@@ -812,7 +817,7 @@ cudaError_t launch_worklist(const int64_t* offsets, const int32_t* indices, uint
     cudaError_t e = cudaFuncSetAttribute(worklist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     worklist_kernel<<<(unsigned)items, kWlThreads, smem, st>>>(offsets, indices, wl, wl_len, BH, Np, n_it, N, pq,
-                                                               stripe_words);
+                                                               stripe_words, cap);
     return cudaGetLastError();
 }
 

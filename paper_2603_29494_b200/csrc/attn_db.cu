@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
             }
             // ---------------------------------------------------------------- epilogue
             // rows that only ever saw masked keys carry m_ref ~ -2^100*scale*log2e: no visible key
-            const float l = (m_ref < -1e28f) ? 0.f : lsum2.x + lsum2.y;
+            const float l = (m_ref < -0x1p99f * sl2) ? 0.f : lsum2.x + lsum2.y;  // scale-aware: masked = -2^100*sl2
             const float inv = l > 0.f ? 1.f / l : 0.f;
             __nv_bfloat16* orow = p.o + (I.bh * p.N + qrow) * D;
             if (I.n_chunks > 0) {  // every PV of the item complete (ODONE parity may be 2 behind here)

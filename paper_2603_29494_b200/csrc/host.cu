@@ -686,10 +686,14 @@ vecattn_status_t vecattn_sparse_fwd(const vecattn_problem_t* p, int32_t pq, cons
     ap->offsets = offsets;
     ap->wl_len = wl_len;
     ap->work_counter = counter;
+    // capacity guard: nnz = offsets[R] beyond the plan's nnz_cap skips the plan and
+    // the attention on the device instead of writing past the workspace
+    ap->d_nnz = offsets + ap->BH * ap->Np;
+    ap->nnz_cap = nnz_cap;
     if (g_timing.enabled) tbegin(false, true);
     tmark(1, cs);
     cudaError_t e = va::launch_worklist(offsets, indices ? indices : reinterpret_cast<const int32_t*>(wl), wl, wl_len,
-                                        ap->BH, ap->Np, ap->n_mt, p->N, pq, cs);
+                                        ap->BH, ap->Np, ap->n_mt, p->N, pq, nnz_cap, cs);
     if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, sizeof(int), cs);
     tmark(2, cs);
     if (e == cudaSuccess) e = va::launch_attn(*ap, (int)p->D, true, attn_grid(ap->total_items), cs);
@@ -794,7 +798,12 @@ vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_selec
     const bool emit = indices && cap > 0;
     // (non-causal only: the causal attention kernel holds all 64K registers of its SM, so a
     // side CTA could not run beside it)
-    SideStream* side = (emit && !p->causal && !getenv("VECATTN_SERIAL_EMIT")) ? side_stream() : nullptr;
+    // (a stream being captured into a CUDA graph keeps the serial order: the library-global
+    // side stream must not be pulled into the caller's capture)
+    cudaStreamCaptureStatus capst = cudaStreamCaptureStatusNone;
+    const bool capturing = cudaStreamIsCapturing(cs, &capst) == cudaSuccess && capst != cudaStreamCaptureStatusNone;
+    SideStream* side =
+        (emit && !p->causal && !capturing && !getenv("VECATTN_SERIAL_EMIT")) ? side_stream() : nullptr;
     tmark(0, cs);
     cudaError_t e = run_select(p, s, q, k, offsets, d_nnz, w, *sp, cs);
     tmark(1, cs);

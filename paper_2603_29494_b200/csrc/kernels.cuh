@@ -112,8 +112,10 @@ struct AttnParams {
     float scale, scale_log2;
 };
 
+// Plan from a CSR; every item skips (wl_len = 0) if offsets[BH*Np] > cap (the plan buffer's capacity).
 cudaError_t launch_worklist(const int64_t* offsets, const int32_t* indices, uint32_t* wl, int32_t* wl_len,
-                            int64_t BH, int64_t Np, int64_t n_it, int64_t N, int32_t pq, cudaStream_t st);
+                            int64_t BH, int64_t Np, int64_t n_it, int64_t N, int32_t pq, int64_t cap,
+                            cudaStream_t st);
 cudaError_t launch_attn(const AttnParams& p, int D, bool gather, int grid, cudaStream_t st);
 // Double-buffered 64-key variant of the gather kernel (attn_db.cu), used for non-causal plans.
 cudaError_t launch_attn_db(const AttnParams& p, int D, int grid, cudaStream_t st);

@@ -124,6 +124,7 @@ def select_naive_into(q, k, mode: str, offsets, indices, cap: int, d_nnz, ws: to
     """Raw vecattn_select_naive call (materialise-then-filter baseline) into caller buffers."""
     lib = load()
     _dev_check(q, k, offsets, indices, d_nnz)
+    _check_io(q, k, offsets=offsets, indices=indices, d_nnz=d_nnz, pq=pq)
     pr = problem(q, k, causal, scale)
     rc = lib.vecattn_select_naive(ctypes.byref(pr), int(pq), NAIVE_MODES[mode], float(alpha), float(top_p), _ptr(q),
                                   _ptr(k), _ptr(offsets), _ptr(indices), int(cap), _ptr(d_nnz), _ptr(ws), ws.numel(),
@@ -190,6 +191,43 @@ def _dev_check(*ts):
             raise ValueError("vecattn: tensors must be contiguous")
 
 
+def _check_io(q, k=None, v=None, o=None, lse=None, offsets=None, indices=None, d_nnz=None, pq=None,
+              cfg=None):
+    """Argument checks the C ABI cannot do on raw pointers: dtypes, shapes,
+    devices and sizes.  A mismatch would otherwise read or write out of bounds on the device."""
+    if q.dim() != 4 or q.dtype != torch.bfloat16:
+        raise ValueError(f"vecattn: q must be bf16 [B,Hq,N,D], got {q.dtype} {tuple(q.shape)}")
+    B, Hq, N, D = q.shape
+    for name, t in (("k", k), ("v", v)):
+        if t is None:
+            continue
+        if t.dtype != torch.bfloat16 or t.dim() != 4 or t.shape[0] != B or t.shape[2] != N or t.shape[3] != D:
+            raise ValueError(f"vecattn: {name} must be bf16 [B,Hkv,N,D] matching q {tuple(q.shape)}, "
+                             f"got {t.dtype} {tuple(t.shape)}")
+        if Hq % t.shape[1] != 0:
+            raise ValueError(f"vecattn: Hq={Hq} is not a multiple of Hkv={t.shape[1]}")
+    if k is not None and v is not None and k.shape != v.shape:
+        raise ValueError(f"vecattn: k {tuple(k.shape)} and v {tuple(v.shape)} differ")
+    if o is not None and (o.dtype != torch.bfloat16 or o.shape != q.shape):
+        raise ValueError(f"vecattn: o must be bf16 {tuple(q.shape)}, got {o.dtype} {tuple(o.shape)}")
+    if lse is not None and (lse.dtype != torch.float32 or tuple(lse.shape) != (B, Hq, N)):
+        raise ValueError(f"vecattn: lse must be float32 {(B, Hq, N)}, got {lse.dtype} {tuple(lse.shape)}")
+    if offsets is not None:
+        if offsets.dtype != torch.int64:
+            raise ValueError("vecattn: offsets must be int64")
+        if pq is not None and offsets.numel() < B * Hq * ((N + pq - 1) // pq) + 1:
+            raise ValueError(f"vecattn: offsets needs B*Hq*N_p+1 = {B * Hq * ((N + pq - 1) // pq) + 1} entries")
+    if indices is not None and indices.dtype != torch.int32:
+        raise ValueError("vecattn: indices must be int32")
+    if d_nnz is not None and (d_nnz.dtype != torch.int64 or d_nnz.numel() < 1):
+        raise ValueError("vecattn: d_nnz must be an int64 device scalar")
+    if cfg is not None and cfg.alpha_per_head is not None and len(cfg.alpha_per_head) != Hq:
+        raise ValueError(f"vecattn: alpha_per_head needs Hq={Hq} entries, got {len(cfg.alpha_per_head)}")
+    for t in (k, v, o, lse, offsets, indices, d_nnz):
+        if t is not None and t.device != q.device:
+            raise ValueError(f"vecattn: every tensor must be on {q.device}, got one on {t.device}")
+
+
 def problem(q: torch.Tensor, k: torch.Tensor, causal: bool, scale: float | None = None) -> Problem:
     B, Hq, N, D = q.shape
     Hkv = k.shape[1]
@@ -237,6 +275,7 @@ class Workspace:
 def pool(q: torch.Tensor, pq: int = 64, stream=None) -> torch.Tensor:
     lib = load()
     _dev_check(q)
+    _check_io(q)
     B, H, N, D = q.shape
     Np = (N + pq - 1) // pq
     qp = torch.empty(B, H, Np, D, dtype=torch.bfloat16, device=q.device)
@@ -254,6 +293,7 @@ def select_into(q, k, cfg: SelectConfig, offsets, indices, cap: int, d_nnz, ws: 
     """Raw vecattn_select call into caller buffers (no host sync)."""
     lib = load()
     _dev_check(q, k, offsets, indices, d_nnz)
+    _check_io(q, k, offsets=offsets, indices=indices, d_nnz=d_nnz, pq=cfg.pq, cfg=cfg)
     pr = problem(q, k, causal, scale)
     sp = cfg.params()
     rc = lib.vecattn_select(ctypes.byref(pr), ctypes.byref(sp), _ptr(q), _ptr(k), _ptr(offsets), _ptr(indices),
@@ -285,6 +325,7 @@ def select(q, k, cfg: SelectConfig, causal: bool = False, scale=None, ws: Worksp
 def debug_scores(q, k, pq: int = 64, ws: Workspace | None = None, stream=None) -> torch.Tensor:
     lib = load()
     _dev_check(q, k)
+    _check_io(q, k)
     B, H, N, D = q.shape
     Np = (N + pq - 1) // pq
     pr = problem(q, k, False)
@@ -305,6 +346,9 @@ def sparse_fwd_into(q, k, v, offsets, indices, pq, o, lse, ws: torch.Tensor, nnz
                     scale=None, stream=None):
     lib = load()
     _dev_check(q, k, v, offsets, indices, o, lse)
+    _check_io(q, k, v, o, lse, offsets=offsets, indices=indices, pq=pq)
+    if indices is not None and indices.numel() < nnz_cap:
+        raise ValueError(f"vecattn: indices has {indices.numel()} entries < nnz_cap={nnz_cap}")
     pr = problem(q, k, causal, scale)
     rc = lib.vecattn_sparse_fwd(ctypes.byref(pr), pq, _ptr(q), _ptr(k), _ptr(v), _ptr(offsets), _ptr(indices),
                                 int(nnz_cap), _ptr(o), _ptr(lse), _ptr(ws), ws.numel(), _stream(stream))
@@ -327,6 +371,7 @@ def sparse_fwd(q, k, v, offsets, indices, pq: int = 64, causal: bool = False, sc
 def dense_fwd_into(q, k, v, o, lse, ws: torch.Tensor, causal: bool, scale=None, stream=None):
     lib = load()
     _dev_check(q, k, v, o, lse)
+    _check_io(q, k, v, o, lse)
     pr = problem(q, k, causal, scale)
     rc = lib.vecattn_dense_fwd(ctypes.byref(pr), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(ws),
                                ws.numel(), _stream(stream))
@@ -351,6 +396,9 @@ def forward_into(q, k, v, cfg: SelectConfig, offsets, indices, cap: int, d_nnz, 
     """Raw vecattn_forward (fused selection + sparse attention) into caller buffers."""
     lib = load()
     _dev_check(q, k, v, offsets, indices, d_nnz, o, lse)
+    _check_io(q, k, v, o, lse, offsets=offsets, indices=indices, d_nnz=d_nnz, pq=cfg.pq, cfg=cfg)
+    if indices is not None and indices.numel() < cap:
+        raise ValueError(f"vecattn: indices has {indices.numel()} entries < cap={cap}")
     pr = problem(q, k, causal, scale)
     sp = cfg.params()
     rc = lib.vecattn_forward(ctypes.byref(pr), ctypes.byref(sp), _ptr(q), _ptr(k), _ptr(v), _ptr(offsets),

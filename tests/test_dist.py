@@ -1,5 +1,5 @@
 """Multi-process (gloo, world_size 2) tests of the head-parallel host logic:
-head partitioning, the padded all-gather of O (C1) and reassembly.
+head partitioning, the group-wise overlapped all-gather of O (C1) and reassembly.
 Per-head compute is the fp64 oracle (test infrastructure), so this runs on CPU."""
 import os
 import socket
@@ -36,41 +36,60 @@ def _free_port():
     return p
 
 
-def _worker(rank, ws, port, H, N, D, out):
+def _head_inputs(h, kvh, N, D):
+    from paper_2603_29494_b200 import synth
+    q = synth.gauss_head(N, D, synth.seed_of(9, 0, h, 0)).double().numpy()
+    k = synth.gauss_head(N, D, synth.seed_of(9, 0, kvh, 1)).double().numpy()
+    v = synth.gauss_head(N, D, synth.seed_of(9, 0, kvh, 2)).double().numpy()
+    return q, k, v
+
+
+def _worker(rank, ws, port, H, Hkv, N, D, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(ws))
     dist.init_process_group("gloo", rank=rank, world_size=ws)
     from oracle import oracle as orc
-    from paper_2603_29494_b200 import synth
     B = 1
-    h0, h1, hmax = bench.head_range(H, ws, rank)
-    o_local = torch.empty(B, h1 - h0, N, D, dtype=torch.float64)
-    for h in range(h0, h1):  # per-head seeded inputs: identical on any rank count
-        q = synth.gauss_head(N, D, synth.seed_of(9, 0, h, 0)).double().numpy()
-        k = synth.gauss_head(N, D, synth.seed_of(9, 0, h, 1)).double().numpy()
-        v = synth.gauss_head(N, D, synth.seed_of(9, 0, h, 2)).double().numpy()
-        o, _ = orc.dense_attn(q, k, v)
-        o_local[0, h - h0] = torch.from_numpy(o)
-    o_pad = torch.zeros(B * hmax * N * D, dtype=torch.float64)
-    o_all = torch.empty(ws, B * hmax * N * D, dtype=torch.float64)
-    bench.allgather_heads(o_local, o_pad, o_all)
-    full = bench.assemble_heads(o_all, B, H, N, D, ws)
+    h0, h1, _ = bench.head_range(H, ws, rank)
+    hg = bench.HeadGather(H, Hkv, B, N, D, ws, rank, torch.float64, "cpu", ngroups=2)
+    rep = H // Hkv
+
+    def compute(g, rng, o_out):  # per-group compute; the group's all-gather runs async meanwhile
+        q0, q1, _, _ = rng
+        for hl in range(q0, q1):
+            h = h0 + hl
+            q, k, v = _head_inputs(h, h // rep, N, D)
+            o, _ = orc.dense_attn(q, k, v)
+            o_out[0, hl - q0] = torch.from_numpy(o)
+
+    hg.run(compute)
+    full = hg.assemble()
     if rank == 0:
         torch.save(full, out)
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("H", [4, 3])
-def test_gloo_allgather_matches_single_rank(tmp_path, H):
+@pytest.mark.parametrize("H,Hkv", [(4, 4), (3, 3), (7, 1), (6, 2)])
+def test_gloo_overlapped_allgather_matches_single_rank(tmp_path, H, Hkv):
+    """Group-wise async all-gather (HeadGather) over 2 ranks: the assembled O is bit-identical
+    to one rank's computation, including uneven (3 over 2) and GQA-cut (7/1, 6/2) splits."""
     N, D = 96, 16
     out = str(tmp_path / "o.pt")
-    mp.spawn(_worker, args=(2, _free_port(), H, N, D, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), H, Hkv, N, D, out), nprocs=2, join=True)
     full = torch.load(out)
     from oracle import oracle as orc
-    from paper_2603_29494_b200 import synth
     for h in range(H):
-        q = synth.gauss_head(N, D, synth.seed_of(9, 0, h, 0)).double().numpy()
-        k = synth.gauss_head(N, D, synth.seed_of(9, 0, h, 1)).double().numpy()
-        v = synth.gauss_head(N, D, synth.seed_of(9, 0, h, 2)).double().numpy()
+        q, k, v = _head_inputs(h, h // (H // Hkv), N, D)
         o, _ = orc.dense_attn(q, k, v)
         np.testing.assert_array_equal(full[0, h].numpy(), o)  # bit-identical to 1-rank
+
+
+def test_kv_groups_cover_local_heads():
+    for H, Hkv in ((24, 24), (28, 4), (40, 40), (28, 28)):
+        for ws in (1, 2, 4, 8):
+            for r in range(ws):
+                h0, h1, _ = bench.head_range(H, ws, r)
+                groups = bench.kv_groups(H, Hkv, ws, r)
+                assert groups[0][0] == 0 and groups[-1][1] == h1 - h0
+                for (a0, a1, b0, b1), (c0, _, d0, _) in zip(groups, groups[1:]):
+                    assert a1 == c0 and b1 == d0 and a1 > a0

@@ -76,3 +76,51 @@ def test_full_size_forward_sampled(wl_name, alpha):
     err = np.abs(od[0, 0].float().cpu().numpy()[rows] - do)
     assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN, (wl_name, "dense", err.max(), err.mean())
     assert np.abs(ld[0, 0].cpu().numpy()[rows] - dl).max() <= LSE_ATOL
+
+
+@pytest.mark.parametrize("mode", ["exact", "topk"])
+def test_full_size_exact_and_topk_sampled(mode):
+    """dit128k (24 heads, N = 131072) with MINS_EXACT (Eq. 3, alpha calibrated to rho = 0.785)
+    and TOPK (keep 21.5% of the keys of every block): sampled pooled rows of three heads vs
+    the oracle under the near-tie rule (TOPK: counts equal the budget), and sampled blocks of
+    attention on the GPU's own index sets."""
+    import bench
+    import paper_2603_29494_b200.vecattn as va
+    va.load()
+    wl = synth.WORKLOADS["dit128k"]
+    dev = torch.device("cuda:0")
+    q, k, v = bench.build_inputs(wl, "video", dev, 0, wl.Hq)
+    pq = 64
+    Np = (wl.N + pq - 1) // pq
+    if mode == "exact":
+        from paper_2603_29494_b200 import calibrate as cal
+        alpha = cal.calibrate_uniform(q, k, va.SelectConfig(mode="exact", pq=pq), 0.785, causal=False)
+        cfg = va.SelectConfig(mode="exact", pq=pq, alpha=alpha)
+        omode, kw = orc.SEL_MINS_EXACT, dict(alpha=alpha)
+    else:
+        cfg = va.SelectConfig(mode="topk", pq=pq, keep_frac=0.215)
+        omode, kw = orc.SEL_TOPK, dict(keep_frac=0.215)
+    o, lse, off, idx = va.forward(q, k, v, cfg, causal=False)
+    qp = va.pool(q, pq)
+    torch.cuda.synchronize()
+    off_h, idx_h = off.cpu().numpy(), idx.cpu().numpy()
+    assert va.validate_selection(off, idx, tuple(q.shape), pq, False) == 0
+    if mode == "topk":
+        budget = int(np.floor(0.215 * wl.N + 0.5))
+        assert np.all(np.diff(off_h) == budget)
+    rng = np.random.default_rng(11)
+    for h in (0, 11, 23):
+        kh, vh, qh = bf16_np(k[0, h]), bf16_np(v[0, h]), bf16_np(q[0, h])
+        rows = np.unique(np.concatenate([[0, Np - 1], rng.choice(Np, 4, replace=False)]))
+        n, nk, ties = compare_selection(off_h, idx_h, bf16_np(qp[0, h]), kh, pq, rows, causal=False, mode=omode,
+                                        bk=16, gk=wl.gk, row_base=h * Np, **kw)
+        assert ties <= 4
+        hoff = off_h[h * Np:(h + 1) * Np + 1] - off_h[h * Np]
+        hidx = idx_h[off_h[h * Np]:off_h[(h + 1) * Np]]
+        blocks = np.unique(np.concatenate([[0, Np - 1], rng.choice(Np, 2, replace=False)]))
+        oo, ol = orc.sparse_attn(qh, kh, vh, hoff, hidx, pq, causal=False, blocks=blocks)
+        rows_q = (blocks[:, None] * pq + np.arange(pq)[None, :]).reshape(-1)
+        og = o[0, h].float().cpu().numpy()[rows_q]
+        err = np.abs(og - oo)
+        assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN, (mode, h, err.max(), err.mean())
+        assert np.abs(lse[0, h].cpu().numpy()[rows_q] - ol).max() <= LSE_ATOL

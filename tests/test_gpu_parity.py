@@ -216,20 +216,23 @@ def test_sparse_full_selection_equals_dense():
         assert (lse - lsed).abs().max().item() <= 1e-3
 
 
-def test_sparse_degenerate_rows_and_empty_blocks():
+@pytest.mark.parametrize("scale", [None, 2e-3])
+def test_sparse_degenerate_rows_and_empty_blocks(scale):
     # causal block 0 selects only its last key -> rows 0..62 see nothing -> O_r = V_r (R6);
-    # a non-causal block with an empty list -> all its rows take V_r.
+    # a non-causal block with an empty list -> all its rows take V_r.  A small caller scale
+    # (2e-3 < 0.0055) checks that degenerate rows are still detected (the masked
+    # score is -2^100 * scale, so the threshold must scale with it).
     N, D, pq = 256, 128, 64
     q, k, v, qd, kd, vd = make("gauss", 1, 1, 1, N, D)
     sets = [[63], [5, 64, 100], [], [0, 200, 255]]
     off = torch.tensor(np.concatenate([[0], np.cumsum([len(s) for s in sets])]), dtype=torch.int64, device=dev())
     idx = torch.tensor(sum(sets, []), dtype=torch.int32, device=dev())
     for causal in (True, False):
-        o, lse = va.sparse_fwd(qd, kd, vd, off, idx, pq=pq, causal=causal)
+        o, lse = va.sparse_fwd(qd, kd, vd, off, idx, pq=pq, causal=causal, scale=scale)
         torch.cuda.synchronize()
         ro, rl = orc.sparse_attn(bf16_np(q[0, 0]), bf16_np(k[0, 0]), bf16_np(v[0, 0]), off.cpu().numpy(),
-                                 idx.cpu().numpy(), pq, causal=causal)
-        check_attn(bf16_np(o[0, 0]), lse[0, 0].cpu().numpy(), ro, rl, f"degenerate causal={causal}")
+                                 idx.cpu().numpy(), pq, causal=causal, scale=scale)
+        check_attn(bf16_np(o[0, 0]), lse[0, 0].cpu().numpy(), ro, rl, f"degenerate causal={causal} scale={scale}")
 
 
 # ------------------------------------------------------------------ fused forward

@@ -213,4 +213,24 @@ def test_sparsity_full_selection_zero():
     N, pq = 256, 64
     off = np.arange(0, 5 * N, N, dtype=np.int64)
     idx = np.tile(np.arange(N, dtype=np.int32), 4)
-    assert orc.sparsity(off, N, pq, causal=False) == 0.0
+    assert orc.sparsity(off, idx, N, pq, causal=False) == 0.0
+
+
+def test_sparsity_hand_computed():
+    """Reading R15, worked by hand.  N = 4, P_q = 2.
+    Non-causal, Idx(0) = {1}, Idx(1) = {0, 2, 3}: kept pairs 2*1 + 2*3 = 8 of 16 -> rho = 1/2.
+    Causal, Idx(0) = {0, 1}, Idx(1) = {0, 3}: row 0 sees {0}, row 1 {0, 1}, row 2 {0} (3 > 2),
+    row 3 {0, 3}: 6 visible pairs of N(N+1)/2 = 10 -> rho = 0.4 (a count of C_i * h_i would
+    give 8 and rho = 0.2: it over-counts the diagonal block).
+    Ragged, N = 5, P_q = 2, non-causal, Idx = {0} | {1, 4} | {2, 3}: 2*1 + 2*2 + 1*2 = 8 of 25."""
+    assert orc.sparsity([0, 1, 4], [1, 0, 2, 3], 4, 2, causal=False) == 0.5
+    assert abs(orc.sparsity([0, 2, 4], [0, 1, 0, 3], 4, 2, causal=True) - 0.4) < 1e-15
+    assert abs(orc.sparsity([0, 1, 3, 5], [0, 1, 4, 2, 3], 5, 2, causal=False) - (1 - 8 / 25)) < 1e-15
+    # full causal selection (every visible key) -> 0
+    N, pq = 7, 3
+    off, idx = [0], []
+    for i in range(3):
+        keys = list(range(min(N, (i + 1) * pq)))
+        idx += keys
+        off.append(len(idx))
+    assert orc.sparsity(off, idx, N, pq, causal=True) == 0.0
