@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libvecattn.so")
-SOURCES = ["pool.cu", "select.cu", "compact.cu", "attn.cu", "attn_db.cu", "naive.cu", "host.cu"]
+SOURCES = ["pool.cu", "select.cu", "compact.cu", "attn.cu", "attn_db.cu", "attn_pair.cu", "naive.cu", "host.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",

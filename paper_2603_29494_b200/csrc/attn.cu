@@ -39,6 +39,7 @@
 #include "attn_plan.cuh"
 
 #include <math.h>
+#include <stdlib.h>
 
 namespace va {
 
@@ -831,11 +832,24 @@ static cudaError_t launch_attn_t(const AttnParams& p, int grid, cudaStream_t st)
     return cudaGetLastError();
 }
 
+bool attn_uses_pair(const AttnParams& p, int D, bool gather) {
+    // The CTA-pair kernel is correct but slower than the double-buffered single-SM kernel on
+    // the dit128k plan (84 vs 74 ms, profiles/ubench_r02.md): opt-in with VECATTN_PAIR=1.
+    if (!gather || p.causal || D != 128) return false;
+    const char* e = getenv("VECATTN_PAIR");
+    return e != nullptr && e[0] == '1';
+}
+
 cudaError_t launch_attn(const AttnParams& p, int D, bool gather, int grid, cudaStream_t st) {
     // Non-causal sparse plans are dominated by chunks of one tile (segments tile 0 / tile 1
     // only), where the double-buffered 64-key kernel (attn_db.cu) is faster; the 128-key
     // ping-pong kernel wins for dense and causal (profiles/sweep_r01.md vs sweep_r01v6.md).
-    if (gather && !p.causal) return launch_attn_db(p, D, grid, st);
+    if (gather && !p.causal) {
+        // D = 128 with VECATTN_PAIR=1: the CTA-pair kernel (attn_pair.cu); otherwise the
+        // single-SM double-buffered kernel (attn_db.cu).
+        if (attn_uses_pair(p, D, gather)) return launch_attn_pair(p, attn_pair_grid(p.total_items, grid_sms()), st);
+        return launch_attn_db(p, D, grid, st);
+    }
     if (D == 128) return gather ? launch_attn_t<128, true>(p, grid, st) : launch_attn_t<128, false>(p, grid, st);
     if (D == 64) return gather ? launch_attn_t<64, true>(p, grid, st) : launch_attn_t<64, false>(p, grid, st);
     return cudaErrorInvalidValue;

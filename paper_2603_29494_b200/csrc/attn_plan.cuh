@@ -13,13 +13,19 @@
 namespace va {
 namespace plan {
 
-// Debug timeline (p.trace != null): CTA 0 records clock64() per chunk and event kind
+// Debug timeline (p.trace != null, [32][4096] int64): CTAs 0 and 1 record %globaltimer (ns) per chunk and event kind
 // (0 K issue, 1 V issue, 2 K landed, 3 V landed, 4/5 PV0/PV1 issued, 6/7 S0 ready/P0 done,
 // 8/9 S1 ready/P1 done) -- scripts/trace_run.py.
 constexpr int kTraceChunks = 4096;
+// %globaltimer (ns), comparable across the SMs of a pair (clock64 is per SM)
+VA_DEV long long globaltimer_ns() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 VA_DEV void trace(const AttnParams& p, int kind, int64_t c) {
-    if (p.trace != nullptr && blockIdx.x == 0 && c < kTraceChunks)
-        p.trace[(int64_t)kind * kTraceChunks + c] = clock64();
+    if (p.trace != nullptr && blockIdx.x < 2 && c < kTraceChunks)  // CTA 1 (the pair's peer): kinds + 16
+        p.trace[(int64_t)(kind + 16 * blockIdx.x) * kTraceChunks + c] = globaltimer_ns();
 }
 
 struct Item {

@@ -653,9 +653,7 @@ static vecattn_status_t attn_common(const vecattn_problem_t* p, const void* q, c
 }
 
 static int attn_grid(int64_t items) {
-    int dev = 0, sms = va::kNumSMsB200;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return (int)std::max<int64_t>(1, std::min<int64_t>(items, sms));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(items, va::grid_sms()));
 }
 
 vecattn_status_t vecattn_sparse_fwd(const vecattn_problem_t* p, int32_t pq, const void* q, const void* k,
@@ -803,7 +801,9 @@ vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_selec
     cudaStreamCaptureStatus capst = cudaStreamCaptureStatusNone;
     const bool capturing = cudaStreamIsCapturing(cs, &capst) == cudaSuccess && capst != cudaStreamCaptureStatusNone;
     SideStream* side =
-        (emit && !p->causal && !capturing && !getenv("VECATTN_SERIAL_EMIT")) ? side_stream() : nullptr;
+        (emit && !p->causal && !capturing && !getenv("VECATTN_SERIAL_EMIT") && !va::attn_uses_pair(*ap, (int)p->D, true))
+            ? side_stream()
+            : nullptr;
     tmark(0, cs);
     cudaError_t e = run_select(p, s, q, k, offsets, d_nnz, w, *sp, cs);
     tmark(1, cs);

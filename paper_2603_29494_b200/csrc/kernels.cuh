@@ -117,6 +117,12 @@ cudaError_t launch_worklist(const int64_t* offsets, const int32_t* indices, uint
                             int64_t BH, int64_t Np, int64_t n_it, int64_t N, int32_t pq, int64_t cap,
                             cudaStream_t st);
 cudaError_t launch_attn(const AttnParams& p, int D, bool gather, int grid, cudaStream_t st);
+// Non-causal sparse attention on CTA pairs (attn_pair.cu, D = 128): grid = 2 x min(items, sms/2).
+int attn_pair_grid(int64_t items, int sms);
+cudaError_t launch_attn_pair(const AttnParams& p, int grid, cudaStream_t st);
+int grid_sms();  // SM count of the current device
+// true if launch_attn runs the pair kernel for this problem (it fills its SMs: no side CTA fits)
+bool attn_uses_pair(const AttnParams& p, int D, bool gather);
 // Double-buffered 64-key variant of the gather kernel (attn_db.cu), used for non-causal plans.
 cudaError_t launch_attn_db(const AttnParams& p, int D, int grid, cudaStream_t st);
 

@@ -18,13 +18,13 @@ else:
     sel = torch.arange(0, N, 2, device=dev)
     idx = sel.int().repeat(H * N // 64)
     off = torch.arange(0, H * N // 64 + 1, device=dev, dtype=torch.int64) * sel.numel()
-tr = torch.zeros(16 * 4096, dtype=torch.int64, device=dev)
+tr = torch.zeros(32 * 4096, dtype=torch.int64, device=dev)
 va.sparse_fwd(q, k, v, off, idx, pq=64)
 torch.cuda.synchronize()
 os.environ["VECATTN_TRACE"] = str(tr.data_ptr())
 va.sparse_fwd(q, k, v, off, idx, pq=64)
 torch.cuda.synchronize()
-t = tr.view(16, 4096).cpu().numpy().astype(np.int64)
+t = tr.view(32, 4096).cpu().numpy().astype(np.int64)
 n = int((t[2] > 0).sum())
 t0 = t[t > 0].min()
 names = ["K_issue", "V_issue", "K_landed", "V_landed", "PV0_issued", "PV1_issued", "S0_ready", "P0_done", "S1_ready", "P1_done"]
