@@ -23,6 +23,7 @@ import argparse
 import json
 import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -69,6 +70,8 @@ def parse():
     ap.add_argument("--cpu-sample-blocks", type=int, default=192)
     ap.add_argument("--cpu-sample-rows", type=int, default=64)
     ap.add_argument("--quick", action="store_true", help="small debug run (no e2e/dense/cpu)")
+    ap.add_argument("--no-context", action="store_true", help="skip the torch SDPA / flash-attn dense timings")
+    ap.add_argument("--no-causal-extra", action="store_true", help="skip the causal vlm128k extra line")
     return ap.parse_args()
 
 
@@ -591,6 +594,16 @@ def run_ours(args):
                "ms_per_step": e2e_ms, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
         del qh, kh, vh, oh_host, qd, kd, vd
 
+    # ---- library kernel launches per step, counted (CUPTI via torch.profiler) over one step
+    launches, launch_names = count_launches(step)
+
+    # ---- external dense context (not the denominator): torch SDPA backends / flash-attn on
+    # the same heads, same protocol (L2 flush, CUDA events)
+    dense_context = None
+    if not args.quick and not args.no_context and ws == 1:
+        dense_context = time_dense_context(q, k, v, causal, flush, stream, total_dense=dense_flops(B * H, N, D, causal),
+                                           ours_ms=dense_ms)
+
     # ---- aggregate results
     sp_tot = torch.tensor([sp_flops, float(int(oh[-1]))], dtype=torch.float64, device=dev)
     if ws > 1:
@@ -616,6 +629,9 @@ def run_ours(args):
     if ws > 1:
         dist.all_reduce(sel_bytes_all)
     peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    # selection GEMM work: 2*D flops per (pooled row, visible key), all local heads
+    vis_keys = Npq * N if not causal else sum(min(N, (i + 1) * pq) for i in range(Npq))  # R5: keys <= L_i
+    sel_flops = 2.0 * D * B * Hl * vis_keys
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp) and args.workload == "dit128k" and ws == 1:
@@ -652,11 +668,16 @@ def run_ours(args):
         "stage_ms": {"select": round(sel_stage_ms, 4), "emit_plan": round(plan_stage_ms, 4),
                      "attention": round(attn_ms, 4),
                      "note": "CUDA events recorded by the library on the launching stream (vecattn_kernel_timing)"},
-        "select_roofline": {"bound": "hbm", "achieved": round(float(sel_bytes_all[0]) / ws / (sel_stage_ms * 1e-3) / 1e9, 1),
-                            "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                            "frac": round(float(sel_bytes_all[0]) / ws / (sel_stage_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
-                            "algorithmic_bytes": int(sel_bytes_all[0] / ws),
-                            "note": "pool + selection GEMM/filter + scan; SURVEY 8(d): tensor/issue-bound at rho >= 0.75"},
+        "select_roofline": {"bound": "tensor", "achieved": round(sel_flops / (sel_stage_ms * 1e-3) / 1e12, 2),
+                            "peak": peak, "unit": "TFLOP/s",
+                            "frac": round(sel_flops / (sel_stage_ms * 1e-3) / 1e12 / peak, 4),
+                            "algorithmic_flops": int(sel_flops),
+                            "hbm": {"achieved": round(float(sel_bytes_all[0]) / ws / (sel_stage_ms * 1e-3) / 1e9, 1),
+                                    "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                    "frac": round(float(sel_bytes_all[0]) / ws / (sel_stage_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
+                                    "algorithmic_bytes": int(sel_bytes_all[0] / ws)},
+                            "note": "pool + pooled-score GEMM (2*D per pooled row x visible key, tcgen05) + Alg.1 "
+                                    "filter epilogue + scan; tensor/issue-bound (SURVEY 8(d)), HBM fraction beside it"},
         "roofline": {"bound": "tensor", "kernel": ("attn_kernel<128,gather>" if causal else "attn_db_kernel<128,gather>") +
                      " (attention kernel alone, vecattn_forward)",
                      "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s",
@@ -666,11 +687,19 @@ def run_ours(args):
                      "algorithmic": "4*D*sum_r |J_r| flops per launch (DESIGN.md 'Rooflines')"},
         "clocks": clocks,
         "e2e": e2e,
-        "gpu_launches": {"alg1": 6, "exact": 7, "topk": 10}[args.mode] * args.steps,
+        "gpu_launches": launches * args.steps,
+        "gpu_launches_note": f"{launches} library kernels per step counted with torch.profiler (CUPTI) over one "
+                             f"step: {launch_names}",
     }
     if dense_ms:
         line["dense_roofline"] = {"achieved": line["dense_tflops"], "peak": peak,
                                   "frac": round(line["dense_tflops"] / peak, 4)}
+    if dense_context is not None:
+        line["dense_context"] = dense_context
+    if rank == 0 and ws == 1 and not args.quick and not args.no_causal_extra and args.workload == "dit128k":
+        del q, k, v, o, lse, ws_fwd, indices, ws_sel, flush
+        torch.cuda.empty_cache()
+        line["causal_vlm128k"] = causal_extra(args, dev, peak)
 
     # ---- CPU baseline: the oracle on a bounded sample of the same workload (rank 0, N=1)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.quick:
@@ -679,6 +708,177 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def count_launches(step):
+    """Kernels of this library launched by one call of `step` (names in namespace va::),
+    from a CUPTI trace (torch.profiler): (count, sorted distinct names)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step()
+        torch.cuda.synchronize()
+    names = [e.name for e in prof.events() if e.device_type.name == "CUDA" and "va::" in e.name]
+    short = sorted({n.split("(")[0].replace("void ", "") for n in names})
+    return len(names), short
+
+
+def time_dense_context(q, k, v, causal, flush, stream, total_dense, ours_ms, reps=2):
+    """Dense attention outside this library on the same [B, H, N, D] bf16 tensors, as context
+    for the in-library denominator: torch SDPA with the cuDNN and the
+    flash backends, and flash_attn (FlashAttention-2, the paper's dense baseline) if it
+    runs on this GPU.  Same protocol as the in-library dense timing."""
+    import torch
+    import torch.nn.functional as F
+    out = {}
+    Hq, Hkv = q.shape[1], k.shape[1]
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    try:
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+        for name, be in (("torch_sdpa_cudnn", SDPBackend.CUDNN_ATTENTION), ("torch_sdpa_flash", SDPBackend.FLASH_ATTENTION)):
+            try:
+                with sdpa_kernel([be]):
+                    ms = timed(lambda: F.scaled_dot_product_attention(q, k, v, is_causal=causal, enable_gqa=Hq != Hkv))
+                out[name] = {"ms": round(ms, 3), "tflops": round(total_dense / (ms * 1e-3) / 1e12, 1)}
+            except Exception as e:  # backend not available for this shape / GPU
+                out[name] = {"error": f"{type(e).__name__}: {str(e).splitlines()[0][:160]}"}
+    except Exception as e:
+        out["torch_sdpa"] = {"error": f"{type(e).__name__}: {str(e)[:160]}"}
+    try:
+        from flash_attn import flash_attn_func
+        qt, kt, vt = (x.transpose(1, 2).contiguous() for x in (q, k, v))  # [B, N, H, D]
+        ms = timed(lambda: flash_attn_func(qt, kt, vt, causal=causal))
+        out["flash_attn2"] = {"ms": round(ms, 3), "tflops": round(total_dense / (ms * 1e-3) / 1e12, 1),
+                              "note": "layout transpose outside the timed region"}
+        del qt, kt, vt
+    except Exception as e:
+        out["flash_attn2"] = {"error": f"{type(e).__name__}: {str(e).splitlines()[0][:160] if str(e) else ''}"}
+    best = min((x["ms"] for x in out.values() if "ms" in x), default=None)
+    out["note"] = ("context only: the speed-up denominator is the in-library dense kernel (dense_ms); "
+                   "best external / in-library = " + (f"{best / ours_ms:.3f}" if best and ours_ms else "n/a"))
+    return out
+
+
+def causal_extra(args, dev, peak):
+    """The causal VLM headline beside the DiT one (SURVEY 8(d) 'report both'): vlm128k
+    (H = 28, GQA 4 KV heads, N = 131072, causal), ALG1 at rho = 0.785, fused forward vs the
+    in-library dense kernel, same timing protocol (L2 flush, CUDA events, median)."""
+    import numpy as np
+    import torch
+    from paper_2603_29494_b200 import synth
+    import paper_2603_29494_b200.vecattn as va
+
+    wl = synth.WORKLOADS["vlm128k"]
+    B, H, Hkv, N, D = wl.B, wl.Hq, wl.Hkv, wl.N, wl.D
+    pq = 64
+    q, k, v = build_inputs(wl, "video", dev, 0, H)
+    cfg = va.SelectConfig(mode="alg1", pq=pq, bk=16, gk=wl.gk)
+    pr = va.problem(q, k, True)
+    Np = (N + pq - 1) // pq
+    R = B * H * Np
+    ws_sel = torch.empty(va.select_workspace_bytes(pr, cfg), dtype=torch.uint8, device=dev)
+    offsets = torch.empty(R + 1, dtype=torch.int64, device=dev)
+    d_nnz = torch.empty(1, dtype=torch.int64, device=dev)
+    tot = H * N * (N + 1) / 2.0
+
+    def rho_of(alpha):  # visible-pair sparsity needs indices; calibrate on C_i * h_i (as the main run)
+        cfg.alpha = alpha
+        va.select_into(q, k, cfg, offsets, None, 0, d_nnz, ws_sel, True)
+        counts = np.diff(offsets.cpu().numpy()).astype(np.float64)
+        i = np.arange(counts.size) % Np
+        h = np.minimum(N, (i + 1) * pq) - i * pq
+        return 1.0 - float((counts * h).sum()) / tot
+
+    lo, hi = 0.0, 1.0
+    while rho_of(hi) > args.rho and hi < 1e4:
+        lo, hi = hi, hi * 2.0
+    for _ in range(30):
+        mid = 0.5 * (lo + hi)
+        r = rho_of(mid)
+        if abs(r - args.rho) < 0.0025:
+            lo = hi = mid
+            break
+        lo, hi = (mid, hi) if r > args.rho else (lo, mid)
+    cfg.alpha = 0.5 * (lo + hi)
+    va.select_into(q, k, cfg, offsets, None, 0, d_nnz, ws_sel, True)
+    cap = int(int(d_nnz.item()) * 1.02) + 1024
+    indices = torch.empty(cap, dtype=torch.int32, device=dev)
+    ws_fwd = torch.empty(va.forward_workspace_bytes(pr, cfg, cap), dtype=torch.uint8, device=dev)
+    o = torch.empty_like(q)
+    lse = torch.empty(B, H, N, dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def fwd():
+        va.forward_into(q, k, v, cfg, offsets, indices, cap, d_nnz, cap, o, lse, ws_fwd, True)
+
+    for _ in range(3):
+        fwd()
+    torch.cuda.synchronize()
+    oh = offsets.cpu().numpy()
+    ih = indices[:int(oh[-1])].cpu().numpy()
+    rho = sparsity(oh, N, pq, Np, True, ih, D)
+    sp_flops = sparse_algo_flops(oh, N, pq, D, True, ih, Np)
+    ts, stages = [], []
+    va.kernel_timing(True)
+    for _ in range(max(3, args.steps)):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fwd()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+        stages.append(va.kernel_timing_last())
+    va.kernel_timing(False)
+    ws_d = torch.empty(256, dtype=torch.uint8, device=dev)
+    od = torch.empty_like(q)
+    dts = []
+    for _ in range(2):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        va.dense_fwd_into(q, k, v, od, None, ws_d, True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dts.append(e0.elapsed_time(e1))
+    ms, dms = statistics.median(ts), statistics.median(dts)
+    attn_ms = statistics.median(x[2] for x in stages)
+    total = dense_flops(B * H, N, D, True)
+    return {"workload": "vlm128k", "B": B, "H": H, "Hkv": Hkv, "N": N, "D": D, "causal": True, "pq": pq,
+            "mode": "alg1", "gk": wl.gk, "alpha": round(cfg.alpha, 5), "rho_achieved": round(float(rho), 5),
+            "ms_per_step": round(ms, 4), "value": round(total / (ms * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+            "dense_ms": round(dms, 3), "speedup_vs_dense": round(dms / ms, 3),
+            "stage_ms": {"select": round(statistics.median(x[0] for x in stages), 4),
+                         "emit_plan": round(statistics.median(x[1] for x in stages), 4), "attention": round(attn_ms, 4)},
+            "roofline": {"bound": "tensor", "kernel": "attn_kernel<128,gather>", "achieved": round(sp_flops / (attn_ms * 1e-3) / 1e12, 2),
+                         "peak": peak, "unit": "TFLOP/s", "frac": round(sp_flops / (attn_ms * 1e-3) / 1e12 / peak, 4)},
+            "note": "same process, after the headline; visible-pair sparsity (reading R15)"}
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
 
 
 def cpu_baseline(args, q, k, v, oh, indices, wl, alpha, cfg, t_budget=None):
@@ -709,6 +909,7 @@ def cpu_baseline(args, q, k, v, oh, indices, wl, alpha, cfg, t_budget=None):
     full_s = H * ((t1 - t0) + (t2 - t1) * Np / rows.size + (t3 - t2) * Np / blocks.size)
     value = dense_flops(H, N, D, wl.causal) / full_s / 1e12
     return {"value": value, "unit": "TFLOP/s", "cores": orc.num_threads(), "kind": "oracle",
+            "cpu_model": cpu_model(),
             "sample": f"head 0 of {H}: pool all rows, select {rows.size}/{Np} pooled rows, Eq.5 on "
                       f"{blocks.size}/{Np} blocks (GPU index sets); measured {t3 - t0:.1f} s, "
                       f"extrapolated x{H} heads, linear in rows/blocks -> {full_s:.0f} s per step",
@@ -776,6 +977,7 @@ def run_reference(args):
         "dtype": "f64", "data": f"synthetic {args.kind.upper()}",
         "config": {"workload": args.workload, "N": N, "D": D, "H": H, "alpha": alpha, "mode": args.mode},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": orc.num_threads(), "kind": "oracle",
+                         "cpu_model": cpu_model(),
                          "sample": f"per step: select + Eq.5 for {nb}/{Np} random blocks of head 0, "
                                    f"extrapolated x{Np // nb} blocks x{H} heads"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -60,7 +60,17 @@ constexpr int kChunk = 128;                 // keys per K/V chunk
 constexpr uint32_t kKeyMask = 0x0FFFFFFFu;  // entry = key | membership << 28
 constexpr uint32_t kPad = 0x0FFFFFFFu;      // meta key for padding lanes (sorts last)
 constexpr uint32_t kNegInfBits = 0xff800000u;
-constexpr int kPolyEvery = 4;  // 1 of every kPolyEvery groups of 4 columns takes exp2 on the FMA pipe
+#ifndef VA_ATTN_POLY_NUM
+#define VA_ATTN_POLY_NUM 1
+#endif
+#ifndef VA_ATTN_POLY_DEN
+#define VA_ATTN_POLY_DEN 4
+#endif
+#ifndef VA_ATTN_POLY_FAST
+#define VA_ATTN_POLY_FAST 0
+#endif
+// groups g (of 4 columns) with g % kPolyDen < kPolyNum take exp2 on the FMA pipe
+constexpr int kPolyNum = VA_ATTN_POLY_NUM, kPolyDen = VA_ATTN_POLY_DEN;
 
 template <int D>
 struct AttnCfg {
@@ -548,8 +558,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                             const float2 xb = unpack_f32x2(
                                 ffma2(pack_f32x2(__uint_as_float(a[t + 2]), __uint_as_float(a[t + 3])), sl2x2, nmx2));
                             float p0, p1, p2, p3;
-                            if ((t >> 2) % kPolyEvery == kPolyEvery - 1) {  // FMA-pipe exp2 (MUFU offload)
-                                const float2 pa = ex2_poly2(xa.x, xa.y), pb = ex2_poly2(xb.x, xb.y);
+                            if ((t >> 2) % kPolyDen >= kPolyDen - kPolyNum) {  // FMA-pipe exp2 (MUFU offload)
+                                const float2 pa = VA_ATTN_POLY_FAST ? ex2_poly2_fast(xa.x, xa.y) : ex2_poly2(xa.x, xa.y);
+                                const float2 pb = VA_ATTN_POLY_FAST ? ex2_poly2_fast(xb.x, xb.y) : ex2_poly2(xb.x, xb.y);
                                 p0 = pa.x, p1 = pa.y, p2 = pb.x, p3 = pb.y;
                             } else {
                                 p0 = ex2(xa.x), p1 = ex2(xa.y), p2 = ex2(xb.x), p3 = ex2(xb.y);
