@@ -11,6 +11,7 @@
 #include <vector>
 #include <limits>
 #include <cmath>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -111,10 +112,21 @@ struct SelectWs {
     uint32_t* tk_prefix;
     uint32_t* tk_krem;
     uint32_t* tk_hist;
+    // windowed TOPK (mode TOPK only)
+    void* ks;            // sampled K rows [B*Hkv][Ns][D]
+    uint32_t *tk_smax, *tk_smin, *tk_cabove, *tk_ncand, *tk_fail;
+    float *tk_top, *tk_invw, *tk_lo, *tk_hi, *tk_cand;
+    int32_t* tk_cidx;
+    int* tk_nfail;
+    int64_t cand_cap;
     size_t total;
 };
 
-SelectWs carve_select(const vecattn_problem_t* p, int32_t pq, void* base) {
+constexpr int kTkStride = 8;         // windowed TOPK: 1 of every 8 keys in the sampled passes
+constexpr int64_t kTkCandSeg = 16384;  // candidate pass key segment
+int64_t tk_cand_cap(const vecattn_problem_t* p) { return std::min<int64_t>(p->N, 16384); }
+
+SelectWs carve_select(const vecattn_problem_t* p, int32_t pq, void* base, bool topk = false) {
     const int64_t BH = p->B * p->Hq, Np = n_pooled(p, pq), R = BH * Np;
     uint8_t* b = static_cast<uint8_t*>(base);
     size_t off = 0;
@@ -134,7 +146,37 @@ SelectWs carve_select(const vecattn_problem_t* p, int32_t pq, void* base) {
     w.tk_krem = reinterpret_cast<uint32_t*>(b + off);
     off += align_up((size_t)R * 4);
     w.tk_hist = reinterpret_cast<uint32_t*>(b + off);
-    off += align_up((size_t)R * 256 * 4);
+    off += align_up((size_t)R * 256 * 4 * (topk ? 2 : 1));  // windowed TOPK: two histogram levels
+    w.ks = nullptr;
+    w.tk_smax = w.tk_smin = w.tk_cabove = w.tk_ncand = w.tk_fail = nullptr;
+    w.tk_top = w.tk_invw = w.tk_lo = w.tk_hi = w.tk_cand = nullptr;
+    w.tk_cidx = nullptr;
+    w.tk_nfail = nullptr;
+    w.cand_cap = 0;
+    if (topk) {
+        const int64_t Ns = (p->N + kTkStride - 1) / kTkStride;
+        w.ks = b + off;
+        off += align_up((size_t)(p->B * p->Hkv * Ns * p->D * 2));
+        uint32_t** u32s[] = {&w.tk_smax, &w.tk_smin, &w.tk_cabove, &w.tk_fail};
+        for (uint32_t** x : u32s) {
+            *x = reinterpret_cast<uint32_t*>(b + off);
+            off += align_up((size_t)R * 4);
+        }
+        w.tk_ncand = reinterpret_cast<uint32_t*>(b + off);  // [R][candidate-pass segments]
+        off += align_up((size_t)R * 4 * (size_t)((p->N + kTkCandSeg - 1) / kTkCandSeg));
+        float** f32s[] = {&w.tk_top, &w.tk_invw, &w.tk_lo, &w.tk_hi};
+        for (float** x : f32s) {
+            *x = reinterpret_cast<float*>(b + off);
+            off += align_up((size_t)R * 4);
+        }
+        w.tk_nfail = reinterpret_cast<int*>(b + off);
+        off += align_up(16);
+        w.cand_cap = tk_cand_cap(p);
+        w.tk_cand = reinterpret_cast<float*>(b + off);
+        off += align_up((size_t)R * (size_t)w.cand_cap * 4);
+        w.tk_cidx = reinterpret_cast<int32_t*>(b + off);
+        off += align_up((size_t)R * (size_t)w.cand_cap * 4);
+    }
     w.total = off;
     return w;
 }
@@ -176,6 +218,7 @@ void plan_segments(const vecattn_problem_t* p, const vecattn_select_params_t* s,
     } else if (epi == va::EPI_MAX || epi == va::EPI_THRESH || epi == va::EPI_SCORES || epi == va::EPI_TOPK_HIST) {
         seg = 16384;  // TOPK histogram passes: per-segment histograms are summed in tk_hist
     }
+    if (epi == va::EPI_TK_CAND) seg = std::min<int64_t>(Nr, kTkCandSeg);  // per-(row, segment) candidate slices
     if (seg > Nr) seg = Nr;
     // few rows (e.g. one GPU's share of the heads): shorter segments until the units fill
     // two waves, keeping segments a multiple of the unit granule and >= 2048 keys
@@ -214,6 +257,22 @@ vecattn_status_t fill_select_params(const vecattn_problem_t* p, const vecattn_se
     sp.tk_prefix = w.tk_prefix;
     sp.tk_krem = w.tk_krem;
     sp.tk_hist = w.tk_hist;
+    sp.N_real = p->N;
+    sp.key_stride = 1;
+    sp.only_failed = 0;
+    sp.tk_smax = w.tk_smax;
+    sp.tk_smin = w.tk_smin;
+    sp.tk_top = w.tk_top;
+    sp.tk_invw = w.tk_invw;
+    sp.tk_lo = w.tk_lo;
+    sp.tk_hi = w.tk_hi;
+    sp.tk_cand = w.tk_cand;
+    sp.tk_cidx = w.tk_cidx;
+    sp.cand_cap = w.cand_cap;
+    sp.tk_cabove = w.tk_cabove;
+    sp.tk_ncand = w.tk_ncand;
+    sp.tk_fail = w.tk_fail;
+    sp.tk_nfail = w.tk_nfail;
     sp.topk = s ? s->topk : 0;
     sp.keep_frac = s ? s->keep_frac : 0.f;
     const float scale = eff_scale(p);
@@ -255,7 +314,7 @@ cudaError_t run_select(const vecattn_problem_t* p, const vecattn_select_params_t
             sp.split = 1;
         }
         sp.pass = pass;
-        if (set_k_map(p, k, epi == va::EPI_TOPK_HIST ? 128 : 256, sp) != VECATTN_OK) return cudaErrorInvalidValue;
+        if (set_k_map(p, k, va::select_bn(epi), sp) != VECATTN_OK) return cudaErrorInvalidValue;
         return va::launch_select(sp, epi, (int)p->D, cs);
     };
     cudaError_t e = va::launch_pool(q, w.qp, sp.BH, p->N, p->D, s->pq, cs);
@@ -269,12 +328,125 @@ cudaError_t run_select(const vecattn_problem_t* p, const vecattn_select_params_t
             if (e == cudaSuccess) e = run(va::EPI_MAX, 0);
             if (e == cudaSuccess) e = run(va::EPI_THRESH, 0);
         } else {
+            // windowed TOPK (select.cu): sampled passes -> window -> one candidate pass -> exact
+            // select; the radix passes below then run only for rows whose window missed
+            // (VECATTN_TOPK_RADIX=1: radix passes for every row, the previous method)
+            const bool windowed = w.tk_cand != nullptr && !getenv("VECATTN_TOPK_RADIX");
+            if (windowed) {
+                const int64_t Ns = (p->N + kTkStride - 1) / kTkStride;
+                e = va::launch_tk_sample_k(k, w.ks, p->B * p->Hkv, p->N, Ns, p->D, kTkStride, cs);
+                if (e == cudaSuccess) e = va::launch_tk_rows(sp, 0, kTkStride, cs);
+                if (e == cudaSuccess) e = cudaMemsetAsync(w.tk_nfail, 0, sizeof(int), cs);
+                SelectParams* ss = new SelectParams(sp);  // sampled passes: K = every kTkStride-th row
+                ss->N = Ns;
+                ss->key_stride = kTkStride;
+                auto run_sampled = [&](int epi, int pass) -> cudaError_t {
+                    plan_segments(p, s, epi, *ss);
+                    // min/max: 4096-key units (atomics merge them); histograms: whole sampled rows
+                    ss->seg_len = epi == va::EPI_TK_SHIST ? (Ns + 255) / 256 * 256
+                                                          : std::min<int64_t>(4096, (Ns + 255) / 256 * 256);
+                    ss->n_seg = (Ns + ss->seg_len - 1) / ss->seg_len;
+                    ss->split = 0;
+                    ss->pass = pass;
+                    if (!tmap_3d(&ss->tm_k, w.ks, (uint64_t)p->D, (uint64_t)Ns, (uint64_t)(p->B * p->Hkv),
+                                 (uint32_t)va::select_bn(epi)))
+                        return cudaErrorInvalidValue;
+                    return va::launch_select(*ss, epi, (int)p->D, cs);
+                };
+                if (e == cudaSuccess) e = run_sampled(va::EPI_TK_MINMAX, 0);
+                if (e == cudaSuccess) e = va::launch_tk_rows(sp, 1, kTkStride, cs);
+                if (e == cudaSuccess) e = cudaMemsetAsync(w.tk_hist, 0, (size_t)R * 256 * 4 * 2, cs);
+                if (e == cudaSuccess) e = run_sampled(va::EPI_TK_SHIST, 0);
+                if (e == cudaSuccess) e = va::launch_tk_rows(sp, 2, kTkStride, cs);
+                if (e == cudaSuccess) e = run_sampled(va::EPI_TK_SHIST, 1);
+                if (e == cudaSuccess) e = va::launch_tk_rows(sp, 3, kTkStride, cs);
+                delete ss;
+                // VECATTN_TOPK_FORCE_FALLBACK=1 (tests): no candidate room -> every row takes the
+                // radix fallback, which must give the same selection
+                const int64_t cap_keep = sp.cand_cap;
+                if (getenv("VECATTN_TOPK_FORCE_FALLBACK")) sp.cand_cap = 0;
+                if (e == cudaSuccess) e = run(va::EPI_TK_CAND, 0);
+                if (e == cudaSuccess) e = va::launch_tk_exact(sp, cs);
+                sp.cand_cap = cap_keep;
+                if (e == cudaSuccess && getenv("VECATTN_TOPK_DEBUG")) {  // diagnostics (scripts only)
+                    cudaStreamSynchronize(cs);
+                    const int64_t nsg = (p->N + kTkCandSeg - 1) / kTkCandSeg;
+                    std::vector<uint32_t> ab(R), nc(R), fl(R), ncs(R * nsg);
+                    std::vector<float> lo(R), hi(R);
+                    int nf = 0;
+                    cudaMemcpy(ab.data(), w.tk_cabove, R * 4, cudaMemcpyDeviceToHost);
+                    cudaMemcpy(ncs.data(), w.tk_ncand, R * nsg * 4, cudaMemcpyDeviceToHost);
+                    for (int64_t r = 0; r < R; ++r) {
+                        nc[r] = 0;
+                        for (int64_t g = 0; g < nsg; ++g) nc[r] += ncs[r * nsg + g];
+                    }
+                    cudaMemcpy(fl.data(), w.tk_fail, R * 4, cudaMemcpyDeviceToHost);
+                    cudaMemcpy(lo.data(), w.tk_lo, R * 4, cudaMemcpyDeviceToHost);
+                    cudaMemcpy(hi.data(), w.tk_hi, R * 4, cudaMemcpyDeviceToHost);
+                    cudaMemcpy(&nf, w.tk_nfail, 4, cudaMemcpyDeviceToHost);
+                    double sn = 0;
+                    uint32_t mx = 0, over = 0;
+                    for (int64_t r = 0; r < R; ++r) {
+                        sn += nc[r];
+                        mx = std::max(mx, nc[r]);
+                        over += nc[r] > (uint32_t)w.cand_cap;
+                    }
+                    fprintf(stderr, "[topk window] rows %lld failed %d overflow %u mean cand %.0f max %u\n", (long long)R, nf,
+                            over, sn / R, mx);
+                    std::vector<uint32_t> smx(4), smn(4), h(512);
+                    std::vector<float> tp(4), iw(4);
+                    cudaMemcpy(smx.data(), w.tk_smax, 16, cudaMemcpyDeviceToHost);
+                    cudaMemcpy(smn.data(), w.tk_smin, 16, cudaMemcpyDeviceToHost);
+                    cudaMemcpy(tp.data(), w.tk_top, 16, cudaMemcpyDeviceToHost);
+                    cudaMemcpy(iw.data(), w.tk_invw, 16, cudaMemcpyDeviceToHost);
+                    cudaMemcpy(h.data(), w.tk_hist, 256 * 4, cudaMemcpyDeviceToHost);
+                    cudaMemcpy(h.data() + 256, w.tk_hist + (size_t)R * 256, 256 * 4, cudaMemcpyDeviceToHost);
+                    uint64_t s1 = 0, s2 = 0;
+                    for (int x = 0; x < 256; ++x) { s1 += h[x]; s2 += h[256 + x]; }
+                    fprintf(stderr, "  row0 smax %08x smin %08x top2 %g invw2 %g hist1 sum %llu hist2 sum %llu\n", smx[0], smn[0],
+                            tp[0], iw[0], (unsigned long long)s1, (unsigned long long)s2);
+                    for (int64_t r = 0; r < R; ++r)
+                        if (fl[r]) {  // dump the first failed row's sample histograms (scripts/topk_window_dbg.py)
+                            std::vector<uint32_t> hh(512), mm(2);
+                            std::vector<float> tt(2);
+                            cudaMemcpy(hh.data(), w.tk_hist + r * 256, 1024, cudaMemcpyDeviceToHost);
+                            cudaMemcpy(hh.data() + 256, w.tk_hist + (R + r) * 256, 1024, cudaMemcpyDeviceToHost);
+                            cudaMemcpy(&mm[0], w.tk_smax + r, 4, cudaMemcpyDeviceToHost);
+                            cudaMemcpy(&mm[1], w.tk_smin + r, 4, cudaMemcpyDeviceToHost);
+                            cudaMemcpy(&tt[0], w.tk_top + r, 4, cudaMemcpyDeviceToHost);
+                            cudaMemcpy(&tt[1], w.tk_invw + r, 4, cudaMemcpyDeviceToHost);
+                            if (FILE* fo = fopen("gpurun_out/topk_fail_row.bin", "wb")) {
+                                fwrite(hh.data(), 4, 512, fo);
+                                fwrite(mm.data(), 4, 2, fo);
+                                fwrite(tt.data(), 4, 2, fo);
+                                fwrite(&lo[r], 4, 1, fo);
+                                fwrite(&hi[r], 4, 1, fo);
+                                fwrite(&ab[r], 4, 1, fo);
+                                fwrite(&nc[r], 4, 1, fo);
+                                fclose(fo);
+                            }
+                            break;
+                        }
+                    int shown = 0;
+                    for (int64_t r = 0; r < R && shown < 8; ++r)
+                        if (fl[r]) {
+                            ++shown;
+                            fprintf(stderr, "  FAILED row %lld (i %lld) above %u ncand %u lo %g hi %g\n", (long long)r,
+                                    (long long)(r % sp.Np), ab[r], nc[r], lo[r], hi[r]);
+                        }
+                }
+                sp.only_failed = 1;  // fallback: radix passes for the rows the window missed
+            }
             for (int pass = 0; pass < 4 && e == cudaSuccess; ++pass) {
                 e = cudaMemsetAsync(w.tk_hist, 0, (size_t)R * 256 * 4, cs);
                 if (e == cudaSuccess) e = run(va::EPI_TOPK_HIST, pass);
                 if (e == cudaSuccess) e = va::launch_topk_pick(sp, cs);
             }
+            // windowed rows already have their bits (the candidate pass wrote the keys above the
+            // window, the exact select the kept candidates) and counts = k; the emit pass runs
+            // for the fallback rows only
             if (e == cudaSuccess) e = run(va::EPI_TOPK_EMIT, 0);
+            sp.only_failed = 0;
         }
     }
     if (e == cudaSuccess) e = va::launch_scan(w.counts, R, offsets, d_nnz, cs);
@@ -568,7 +740,7 @@ vecattn_status_t vecattn_pool(const vecattn_problem_t* p, int32_t pq, const void
 
 size_t vecattn_select_workspace_bytes(const vecattn_problem_t* p, const vecattn_select_params_t* s) {
     if (check_problem(p) != VECATTN_OK || !s || (s->pq != 64 && s->pq != 128)) return 0;
-    return carve_select(p, s->pq, nullptr).total;
+    return carve_select(p, s->pq, nullptr, s->mode == VECATTN_SEL_TOPK).total;
 }
 
 vecattn_status_t vecattn_select(const vecattn_problem_t* p, const vecattn_select_params_t* s, const void* q,
@@ -578,11 +750,11 @@ vecattn_status_t vecattn_select(const vecattn_problem_t* p, const vecattn_select
     if (st != VECATTN_OK) return st;
     if (!q || !k || !offsets || !d_nnz || cap < 0 || (cap > 0 && !indices)) return VECATTN_ERR_INVALID_ARGUMENT;
     if (!aligned16(q) || !aligned16(k)) return VECATTN_ERR_SHAPE;
-    const SelectWs need = carve_select(p, s->pq, nullptr);
+    const SelectWs need = carve_select(p, s->pq, nullptr, s->mode == VECATTN_SEL_TOPK);
     if (!ws || ws_bytes < need.total) return VECATTN_ERR_WORKSPACE;
     if (!aligned16(ws)) return VECATTN_ERR_SHAPE;
     cudaStream_t cs = (cudaStream_t)stream;
-    const SelectWs w = carve_select(p, s->pq, ws);
+    const SelectWs w = carve_select(p, s->pq, ws, s->mode == VECATTN_SEL_TOPK);
     SelectParams* sp = new SelectParams;
     st = fill_select_params(p, s, s->pq, k, w, *sp);
     if (st != VECATTN_OK) { delete sp; return st; }
@@ -750,7 +922,7 @@ vecattn_status_t vecattn_validate_selection(const vecattn_problem_t* p, int32_t 
 size_t vecattn_forward_workspace_bytes(const vecattn_problem_t* p, const vecattn_select_params_t* s,
                                        int64_t nnz_cap) {
     if (check_problem(p) != VECATTN_OK || !s || (s->pq != 64 && s->pq != 128) || nnz_cap < 0) return 0;
-    return carve_select(p, s->pq, nullptr).total + vecattn_sparse_workspace_bytes(p, s->pq, nnz_cap);
+    return carve_select(p, s->pq, nullptr, s->mode == VECATTN_SEL_TOPK).total + vecattn_sparse_workspace_bytes(p, s->pq, nnz_cap);
 }
 
 vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_select_params_t* s, const void* q,
@@ -766,7 +938,7 @@ vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_selec
     if (!ws || ws_bytes < need) return VECATTN_ERR_WORKSPACE;
     if (!aligned16(ws)) return VECATTN_ERR_SHAPE;
     cudaStream_t cs = (cudaStream_t)stream;
-    const SelectWs w = carve_select(p, s->pq, ws);
+    const SelectWs w = carve_select(p, s->pq, ws, s->mode == VECATTN_SEL_TOPK);
     uint8_t* b = static_cast<uint8_t*>(ws) + w.total;
     SelectParams* sp = new SelectParams;
     AttnParams* ap = new AttnParams;

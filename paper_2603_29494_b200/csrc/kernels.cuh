@@ -24,6 +24,9 @@ enum SelectEpi : int {
     EPI_TOPK_HIST = 3, // TOPK radix pass (8-bit digit `pass`)
     EPI_TOPK_EMIT = 4, // TOPK: keep key > theta, plus the first k_rem ties in index order
     EPI_SCORES = 5,    // debug: dump raw fp32 accumulators
+    EPI_TK_MINMAX = 6, // TOPK window, sampled keys: row max / min -> tk_smax / tk_smin (ordered u32)
+    EPI_TK_SHIST = 7,  // TOPK window, sampled keys: 256-bin histogram of round((top - s) * invw)
+    EPI_TK_CAND = 8,   // TOPK window, all keys: count s > hi, collect s in [lo, hi] (whole rows)
 };
 
 struct SelectParams {
@@ -48,13 +51,42 @@ struct SelectParams {
     int32_t pass;                  // TOPK pass 0..3
     int64_t topk;                  // TOPK budget
     float keep_frac;
+    // TOPK window selection (select.cu "windowed TOPK"): the sampled passes run on a copy of
+    // every key_stride-th K row (p.N = sampled keys, N_real = the problem's N)
+    int64_t N_real;
+    int32_t key_stride;            // 1, or the sampling stride of the sampled passes
+    int32_t only_failed;           // EPI_TOPK_HIST / EMIT / pick: rows with tk_fail set only (fallback)
+    uint32_t* tk_smax;             // [R] ordered keys of the sampled row max / min
+    uint32_t* tk_smin;
+    float* tk_top;                 // [R] SHIST binning: bin = round((tk_top - s) * tk_invw)
+    float* tk_invw;
+    float* tk_lo;                  // [R] candidate window [lo, hi]
+    float* tk_hi;
+    float* tk_cand;                // [R][cand_cap] window scores
+    int32_t* tk_cidx;              // [R][cand_cap] their key indices (ascending within a segment slice)
+    int64_t cand_cap;
+    uint32_t* tk_cabove;           // [R] visible scores > hi
+    uint32_t* tk_ncand;            // [R] visible scores in [lo, hi]
+    uint32_t* tk_fail;             // [R] 1: the window missed the k-th largest (fallback radix)
+    int* tk_nfail;                 // rows with tk_fail
     float alpha_raw[1024];         // per q head: alpha / scale (raw-accumulator units)
 };
 
 cudaError_t launch_select(const SelectParams& p, int epi, int D, cudaStream_t st);
+int select_bn(int epi);  // key tile (tensor-map box rows) of a selection epilogue
 // TOPK: after a histogram pass, per row: the digit bin holding the k_rem-th largest remaining
 // key -> tk_prefix <<= 8 | bin, tk_krem -= keys in higher bins.
 cudaError_t launch_topk_pick(const SelectParams& p, cudaStream_t st);
+// Windowed TOPK (few passes over sampled keys, one candidate pass, an exact select over the
+// candidates; fallback to the radix passes for rows whose window missed):
+// every key_stride-th row of K -> ks [B*Hkv][Ns][D]
+cudaError_t launch_tk_sample_k(const void* k, void* ks, int64_t BHkv, int64_t N, int64_t Ns, int64_t D, int stride,
+                               cudaStream_t st);
+// stage 0: init per-row state; 1: level-1 binning from the sampled min/max; 2: level-2 binning
+// inside the level-1 bin of the sampled k-th largest; 3: the candidate window [lo, hi]
+cudaError_t launch_tk_rows(const SelectParams& p, int stage, int stride, cudaStream_t st);
+// exact k-th largest among the window candidates -> tk_prefix / tk_krem, or tk_fail
+cudaError_t launch_tk_exact(const SelectParams& p, cudaStream_t st);
 
 // ---------------------------------------------------------------------- compaction
 // offsets[r+1] = sum counts[0..r]; d_nnz = total.

@@ -37,7 +37,7 @@ namespace {
 // the TOPK histogram passes, whose two warp sets take alternate 64-key chunks of every tile
 // and update the same per-row histogram with shared-memory atomics.
 template <int EPI>
-constexpr int epi_warps() { return EPI == EPI_TOPK_HIST ? 8 : 4; }
+constexpr int epi_warps() { return (EPI == EPI_TOPK_HIST || EPI == EPI_TK_SHIST) ? 8 : 4; }
 template <int EPI>
 constexpr int sel_threads() { return 64 + 32 * epi_warps<EPI>(); }
 
@@ -46,7 +46,8 @@ struct SelCfg {
     static constexpr int kCB = D / 64;                       // 128-byte column blocks
     static constexpr int kQBytes = kCB * 128 * 128;          // Q_p tile
     static constexpr int kKStageBytes = kCB * BN * 128;      // one K tile
-    static constexpr int kHistBytes = (EPI == EPI_TOPK_HIST) ? 256 * 128 * 4 : 0;
+    static constexpr int kHistBytes = (EPI == EPI_TOPK_HIST || EPI == EPI_TK_SHIST) ? 256 * 128 * 4
+                                      : (EPI == EPI_TK_CAND ? 64 * 128 * 4 : 0);  // CAND: score staging
     static constexpr int kOffQ = 0;
     static constexpr int kOffK = kQBytes;
     static constexpr int kOffHist = kOffK + STAGES * kKStageBytes;
@@ -73,7 +74,9 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
     const int64_t bh = unit / (p.n_seg * p.n_mt);
     const int64_t m0 = mt * 128;
     const int64_t row_hi = min(p.Np, m0 + 128);  // exclusive
-    const int64_t kend_tile = p.causal ? min(p.N, row_hi * (int64_t)p.pq) : p.N;
+    // sampled TOPK passes: key j of this pass is real key j * stride (R5 visibility on real keys)
+    const int64_t stride = p.key_stride > 1 ? p.key_stride : 1;
+    const int64_t kend_tile = p.causal ? min(p.N, (min(p.N_real, row_hi * (int64_t)p.pq) + stride - 1) / stride) : p.N;
     const int64_t k_begin = seg * p.seg_len;
     const int64_t k_end = min(k_begin + p.seg_len, kend_tile);
     if (k_begin >= k_end) return;  // uniform: causal units above the diagonal
@@ -81,6 +84,15 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
     const int64_t b = bh / p.Hq;
     const int64_t h = bh % p.Hq;
     const int64_t bh_kv = b * p.Hkv + h / (p.Hq / p.Hkv);
+    if constexpr (EPI == EPI_TOPK_HIST || EPI == EPI_TOPK_EMIT) {
+        // fallback of the windowed TOPK: only tiles with a row whose window missed
+        if (p.only_failed) {
+            if (*p.tk_nfail == 0) return;
+            const int64_t rr = m0 + threadIdx.x;
+            const int f = (threadIdx.x < 128 && rr < row_hi) ? (int)p.tk_fail[bh * p.Np + rr] : 0;
+            if (!__syncthreads_or(f)) return;
+        }
+    }
 
     uint8_t* sQ = smem + C::kOffQ;
     uint8_t* sK = smem + C::kOffK;
@@ -165,9 +177,11 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
         const int eset = ((int)warp - 2) >> 2;     // epilogue warp set (TOPK_HIST: 2 sets)
         const int r = (int)(quad * 32 + lane);
         const int64_t i = m0 + r;                  // pooled row within head
-        const bool row_ok = i < p.Np;
         const int64_t grow = bh * p.Np + i;        // global row id
-        const int64_t vis_end = p.causal ? min(p.N, (i + 1) * (int64_t)p.pq) : p.N;
+        const bool row_ok = i < p.Np && !((EPI == EPI_TOPK_HIST || EPI == EPI_TOPK_EMIT) && p.only_failed &&
+                                          p.tk_fail[grow] == 0u);
+        const int64_t vis_real = p.causal ? min(p.N_real, (i + 1) * (int64_t)p.pq) : p.N_real;
+        const int64_t vis_end = (vis_real + stride - 1) / stride;  // visible keys of this pass
         const float alpha_raw = p.alpha_raw[h];
         const int64_t G = (int64_t)p.bk * (int64_t)p.gk;
         int64_t next_reset = k_begin;              // Alg. 1 group boundaries (multiples of G)
@@ -181,6 +195,28 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
             next_reset = (k_begin + G - 1) / G * G;
         }
         float thr_fixed = 0.f;
+        float mn_run = INFINITY;                   // EPI_TK_MINMAX row min
+        float tk_a = 0.f, tk_b = 0.f;              // SHIST: top*invw, invw; CAND: lo, hi
+        uint32_t above = 0, ncand = 0;             // CAND counters
+        if constexpr (EPI == EPI_TK_SHIST) {
+            if (row_ok) {
+                tk_b = p.tk_invw[grow];
+                tk_a = p.tk_top[grow] * tk_b;
+            }
+            if (eset == 0)
+                for (int bin = 0; bin < 256; ++bin) reinterpret_cast<uint32_t*>(smem + C::kOffHist)[bin * 128 + r] = 0u;
+            named_bar_sync(1, 32 * epi_warps<EPI>());  // zeroed before either warp set updates it
+        }
+        if constexpr (EPI == EPI_TK_CAND) {
+            if (row_ok) {
+                tk_a = p.tk_lo[grow];
+                tk_b = p.tk_hi[grow];
+            }
+        }
+        // CAND: this (row, key segment)'s candidate slice; subcap = cand_cap / n_seg
+        const int64_t subcap = (EPI == EPI_TK_CAND) ? p.cand_cap / p.n_seg : 0;
+        float* cand_row = (EPI == EPI_TK_CAND) ? p.tk_cand + grow * p.cand_cap + seg * subcap : nullptr;
+        int32_t* cidx_row = (EPI == EPI_TK_CAND) ? p.tk_cidx + grow * p.cand_cap + seg * subcap : nullptr;
         uint32_t tk_prefix = 0, tk_krem = 0, tk_taken = 0;
         unsigned long long cnt = 0;
         uint32_t* hist = reinterpret_cast<uint32_t*>(smem + C::kOffHist);
@@ -192,10 +228,10 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
             if (row_ok) {
                 if (EPI == EPI_TOPK_HIST && p.pass == 0) {
                     int64_t ki;
-                    if (p.topk > 0) ki = min(p.topk, vis_end);
+                    if (p.topk > 0) ki = min(p.topk, vis_real);
                     else {
-                        ki = (int64_t)floor((double)p.keep_frac * (double)vis_end + 0.5);
-                        ki = max((int64_t)1, min(ki, vis_end));
+                        ki = (int64_t)floor((double)p.keep_frac * (double)vis_real + 0.5);
+                        ki = max((int64_t)1, min(ki, vis_real));
                     }
                     tk_prefix = 0;
                     tk_krem = (uint32_t)ki;
@@ -335,6 +371,94 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
                         w0 &= nvis >= 32 ? 0xffffffffu : ((1u << nvis) - 1u);
                         w1 &= nvis >= 64 ? 0xffffffffu : (nvis <= 32 ? 0u : ((1u << (nvis - 32)) - 1u));
                     }
+                } else if constexpr (EPI == EPI_TK_MINMAX) {
+                    float a = -INFINITY, b2 = -INFINITY, c2 = INFINITY, d2 = INFINITY;
+                    if (nvis == 64) {
+#pragma unroll
+                        for (int j = 0; j < 64; j += 4) {
+                            a = fmax3(a, v[j], v[j + 1]);
+                            b2 = fmax3(b2, v[j + 2], v[j + 3]);
+                            c2 = fminf(fminf(c2, v[j]), v[j + 1]);
+                            d2 = fminf(fminf(d2, v[j + 2]), v[j + 3]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 64; ++j) {
+                            if (j < nvis) {
+                                a = fmaxf(a, v[j]);
+                                c2 = fminf(c2, v[j]);
+                            }
+                        }
+                    }
+                    m_run = fmaxf(m_run, fmaxf(a, b2));
+                    mn_run = fminf(mn_run, fminf(c2, d2));
+                } else if constexpr (EPI == EPI_TK_SHIST) {
+                    // bin = round((top - s) * invw): round-to-nearest by the 1.5*2^23 magic add,
+                    // the integer read from the mantissa; bins outside [0, 255] are skipped
+                    uint32_t* hcol = hist + r;
+#pragma unroll
+                    for (int j = 0; j < 64; ++j) {
+                        const float t = fmaf(v[j], -tk_b, tk_a) + 12582912.f;
+                        const uint32_t bin = (uint32_t)(__float_as_int(t) - 0x4B400000);
+                        if (j < nvis && bin < 256u) atomicAdd(hcol + bin * 128, 1u);
+                    }
+                } else if constexpr (EPI == EPI_TK_CAND) {
+                    // above = s > hi, inside = lo <= s <= hi, as sign bits of hi - s and s - lo
+                    // (the ALG1 trick; +-inf bounds give +inf differences), then predicated stores
+                    uint32_t ab0 = 0u, ab1 = 0u, lo0 = 0u, lo1 = 0u;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 2) {
+                        const float2 ha = fadd2(make_float2(tk_b, tk_b), make_float2(-v[j], -v[j + 1]));
+                        const float2 hb = fadd2(make_float2(tk_b, tk_b), make_float2(-v[32 + j], -v[33 + j]));
+                        const float2 la = fadd2(make_float2(v[j], v[j + 1]), make_float2(-tk_a, -tk_a));
+                        const float2 lb = fadd2(make_float2(v[32 + j], v[33 + j]), make_float2(-tk_a, -tk_a));
+                        ab0 = __funnelshift_l(__float_as_uint(ha.x), ab0, 1);
+                        ab0 = __funnelshift_l(__float_as_uint(ha.y), ab0, 1);
+                        ab1 = __funnelshift_l(__float_as_uint(hb.x), ab1, 1);
+                        ab1 = __funnelshift_l(__float_as_uint(hb.y), ab1, 1);
+                        lo0 = __funnelshift_l(__float_as_uint(la.x), lo0, 1);
+                        lo0 = __funnelshift_l(__float_as_uint(la.y), lo0, 1);
+                        lo1 = __funnelshift_l(__float_as_uint(lb.x), lo1, 1);
+                        lo1 = __funnelshift_l(__float_as_uint(lb.y), lo1, 1);
+                    }
+                    const uint32_t vm0 = nvis >= 32 ? 0xffffffffu : ((1u << nvis) - 1u);
+                    const uint32_t vm1 = nvis >= 64 ? 0xffffffffu : (nvis <= 32 ? 0u : ((1u << (nvis - 32)) - 1u));
+                    ab0 = __brev(ab0) & vm0;
+                    ab1 = __brev(ab1) & vm1;
+                    const uint32_t in0 = ~(ab0 | __brev(lo0)) & vm0;
+                    const uint32_t in1 = ~(ab1 | __brev(lo1)) & vm1;
+                    above += __popc(ab0) + __popc(ab1);
+                    // extraction: the 64 scores go to a column-major shared stage (conflict-free:
+                    // lanes are consecutive rows), then each thread walks its set bits (~4% of
+                    // scores) reading the stage with a dynamic index
+                    float* stg = reinterpret_cast<float*>(hist) + r;
+                    if ((in0 | in1) != 0u) {
+#pragma unroll
+                        for (int j = 0; j < 64; ++j) stg[j * 128] = v[j];
+                        const uint32_t cap = (uint32_t)subcap;
+                        uint32_t m = in0;
+                        while (m) {
+                            const int j = __ffs(m) - 1;
+                            m &= m - 1u;
+                            if (ncand < cap) {
+                                cand_row[ncand] = stg[j * 128];
+                                cidx_row[ncand] = (int32_t)(kc + j);
+                            }
+                            ++ncand;
+                        }
+                        m = in1;
+                        while (m) {
+                            const int j = 32 + __ffs(m) - 1;
+                            m &= m - 1u;
+                            if (ncand < cap) {
+                                cand_row[ncand] = stg[j * 128];
+                                cidx_row[ncand] = (int32_t)(kc + j);
+                            }
+                            ++ncand;
+                        }
+                    }
+                    w0 = ab0;  // keys above the window are kept whatever the k-th largest is
+                    w1 = ab1;
                 } else if constexpr (EPI == EPI_TOPK_HIST) {
                     // branch-free: invisible keys are masked by a predicate, the prefix test of
                     // passes > 0 and the histogram update are predicated shared-memory atomics
@@ -386,7 +510,7 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
             tc_fence_before();
             mbar_arrive(&acc_empty[buf]);
 
-            if constexpr (EPI == EPI_ALG1 || EPI == EPI_THRESH || EPI == EPI_TOPK_EMIT) {
+            if constexpr (EPI == EPI_ALG1 || EPI == EPI_THRESH || EPI == EPI_TOPK_EMIT || EPI == EPI_TK_CAND) {
                 if (row_ok) {
                     uint32_t* dst = p.bitmask + grow * p.words_per_row + key0 / 32;
 #pragma unroll
@@ -398,13 +522,34 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
             }
         }
 
-        if constexpr (EPI == EPI_TOPK_HIST) named_bar_sync(1, 32 * epi_warps<EPI>());  // both sets' updates done
+        if constexpr (EPI == EPI_TOPK_HIST || EPI == EPI_TK_SHIST)
+            named_bar_sync(1, 32 * epi_warps<EPI>());  // both sets' updates done
         if (row_ok) {
             if constexpr (EPI == EPI_ALG1 || EPI == EPI_THRESH || EPI == EPI_TOPK_EMIT) {
                 if (cnt) atomicAdd(&p.counts[grow], cnt);
             } else if constexpr (EPI == EPI_MAX) {
                 if (p.split) p.segmax[grow * p.n_seg + seg] = f32_order_key(m_run);
                 else if (m_run > -INFINITY) atomicMax(&p.rowmax[grow], f32_order_key(m_run));
+            } else if constexpr (EPI == EPI_TK_MINMAX) {
+                if (m_run > -INFINITY) {
+                    atomicMax(&p.tk_smax[grow], f32_order_key(m_run));
+                    atomicMin(&p.tk_smin[grow], f32_order_key(mn_run));
+                }
+            } else if constexpr (EPI == EPI_TK_CAND) {
+                if (above) atomicAdd(&p.tk_cabove[grow], above);
+                p.tk_ncand[grow * p.n_seg + seg] = ncand;
+            } else if constexpr (EPI == EPI_TK_SHIST) {
+                uint32_t* gh = p.tk_hist + ((int64_t)p.pass * p.BH * p.Np + grow) * 256;
+                if (p.n_seg == 1) {  // the whole sampled row in this unit: plain 16-B stores, half per warp set
+                    for (int bin = 128 * eset; bin < 128 * eset + 128; bin += 4)
+                        *reinterpret_cast<uint4*>(gh + bin) = make_uint4(hist[bin * 128 + r], hist[(bin + 1) * 128 + r],
+                                                                         hist[(bin + 2) * 128 + r], hist[(bin + 3) * 128 + r]);
+                } else {
+                    for (int bin = 128 * eset; bin < 128 * eset + 128; ++bin) {
+                        const uint32_t hc = hist[bin * 128 + r];
+                        if (hc) atomicAdd(gh + bin, hc);
+                    }
+                }
             } else if constexpr (EPI == EPI_TOPK_HIST) {
                 // this key segment's counts -> the row's histogram in global memory (the two
                 // warp sets flush half of the bins each; most bins are empty)
@@ -429,6 +574,7 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
 __global__ void __launch_bounds__(256) topk_pick_kernel(const __grid_constant__ SelectParams p) {
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= p.BH * p.Np) return;
+    if (p.only_failed && p.tk_fail[row] == 0u) return;
     const int64_t i = row % p.Np;
     const int64_t vis_end = p.causal ? min(p.N, (i + 1) * (int64_t)p.pq) : p.N;
     uint32_t prefix, krem;
@@ -483,11 +629,14 @@ static cudaError_t launch_sel_d(const SelectParams& p, int epi, cudaStream_t st)
         case EPI_TOPK_HIST: return launch_sel_t<D, 128, 2, EPI_TOPK_HIST>(p, st);
         case EPI_TOPK_EMIT: return launch_sel_t<D, 256, 3, EPI_TOPK_EMIT>(p, st);
         case EPI_SCORES: return launch_sel_t<D, 256, 3, EPI_SCORES>(p, st);
+        case EPI_TK_MINMAX: return launch_sel_t<D, 256, 3, EPI_TK_MINMAX>(p, st);
+        case EPI_TK_SHIST: return launch_sel_t<D, 128, 2, EPI_TK_SHIST>(p, st);
+        case EPI_TK_CAND: return launch_sel_t<D, 128, 2, EPI_TK_CAND>(p, st);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int select_bn(int epi) { return epi == EPI_TOPK_HIST ? 128 : 256; }
+int select_bn(int epi) { return (epi == EPI_TOPK_HIST || epi == EPI_TK_SHIST || epi == EPI_TK_CAND) ? 128 : 256; }
 
 cudaError_t launch_select(const SelectParams& p, int epi, int D, cudaStream_t st) {
     if (D == 128) return launch_sel_d<128>(p, epi, st);
@@ -499,6 +648,276 @@ cudaError_t launch_topk_pick(const SelectParams& p, cudaStream_t st) {
     const int64_t R = p.BH * p.Np;
     if (R <= 0) return cudaSuccess;
     topk_pick_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+// ============================================================================ windowed TOPK
+// The radix TOPK above needs 4 histogram passes that touch every score (~10 ms each at dit128k).
+// Windowed TOPK: estimate the k-th largest score of each row from a 1-in-8 sample of the keys
+// (two cheap sampled passes: min/max, then a 256-bin histogram, refined once inside the bin
+// that holds the sample's k-th largest), take a window [lo, hi] around it wide enough for the
+// sampling error (6 sigma of the binomial rank), and make ONE full pass that counts the scores
+// above hi and collects those inside the window.  The exact k-th largest is then selected
+// among the candidates; rows where the window missed it (or overflowed) fall back to the radix
+// passes.  The result (tk_prefix = order key of the k-th largest, tk_krem = ties to take) is
+// the same state the radix passes produce, so the emit pass and reading R12 are unchanged.
+
+__global__ void tk_sample_k_kernel(const uint4* __restrict__ k, uint4* __restrict__ ks, int64_t BHkv, int64_t N,
+                                   int64_t Ns, int64_t D, int stride) {
+    const int64_t per_row = D / 8;  // uint4 per row
+    const int64_t total = BHkv * Ns * per_row;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = x % per_row, js = (x / per_row) % Ns, bh = x / (per_row * Ns);
+        // one key per group of `stride`, at a hashed offset: a fixed offset would sample the same
+        // position of every period-`stride` structure of the sequence (video patches are 8 wide)
+        const uint32_t hsh = (uint32_t)js * 2654435761u;
+        int64_t j = js * stride + (int64_t)((hsh >> 16) % (uint32_t)stride);
+        if (j >= N) j = N - 1;
+        ks[x] = k[(bh * N + j) * per_row + c];
+    }
+}
+
+namespace {
+VA_DEV int64_t tk_budget(const SelectParams& p, int64_t vis_real) {  // k_i (reading R12)
+    int64_t ki;
+    if (p.topk > 0) ki = min(p.topk, vis_real);
+    else {
+        ki = (int64_t)floor((double)p.keep_frac * (double)vis_real + 0.5);
+        ki = max((int64_t)1, min(ki, vis_real));
+    }
+    return ki;
+}
+}  // namespace
+
+// stage 0: init; 1: level-1 binning over [smin, smax]; 2: level-2 binning inside the level-1
+// bin that holds the sample's k-th largest; 3: the window [lo, hi] from both histograms.
+// Bin b of a level covers s with round((top - s) * invw) == b, i.e. s in [top - (b+.5)/invw,
+// top - (b-.5)/invw]; boundaries are widened by a relative 2^-16 (the exact counts of the
+// candidate pass decide, so a wider window only costs candidates).
+__global__ void __launch_bounds__(256) tk_rows_kernel(const __grid_constant__ SelectParams p, int stage, int stride) {
+    const int64_t R = p.BH * p.Np;
+    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= R) return;
+    if (stage == 0) {
+        p.tk_smax[row] = 0u;
+        p.tk_smin[row] = 0xFFFFFFFFu;
+        p.tk_fail[row] = 0u;
+        p.tk_cabove[row] = 0u;
+        return;
+    }
+    const int64_t i = row % p.Np;
+    const int64_t vis_real = p.causal ? min(p.N_real, (i + 1) * (int64_t)p.pq) : p.N_real;
+    const int64_t ns = (vis_real + stride - 1) / stride;  // visible sampled keys
+    const float smax = f32_from_order_key(p.tk_smax[row]), smin = f32_from_order_key(p.tk_smin[row]);
+    if (stage == 1) {
+        const float w = smax - smin;
+        p.tk_top[row] = smax;
+        p.tk_invw[row] = w > 0.f ? 255.f / w : 0.f;
+        return;
+    }
+    const double ki = (double)tk_budget(p, vis_real);
+    const double ks = ki * (double)ns / (double)vis_real;  // the k-th largest's rank in the sample
+    const uint32_t* h1 = p.tk_hist + row * 256;
+    // level-1 binning (stage 1's, recomputed: tk_top / tk_invw hold level 2 after stage 2)
+    const float top1 = smax, invw1 = (smax - smin) > 0.f ? 255.f / (smax - smin) : 0.f;
+    // window ranks [ks - d, ks + d] in the sample, d = 6 sigma + 4 (binomial rank of a sample quantile)
+    const double pr = min(1.0, ki / (double)vis_real);
+    const double d = 6.0 * sqrt((double)ns * pr * (1.0 - pr)) + 8.0;
+    const double r_lo = ks - d, r_hi = ks + d;
+    if (stage == 2) {
+        // level-1 bins ba..bb hold sample ranks r_lo..r_hi (counted from the top: bin 0 = the
+        // largest); level 2 re-bins exactly that value range into 256 sub-bins
+        double cum = 0.0;
+        int ba = -1, bb = 255;
+        for (int x = 0; x < 256; ++x) {
+            cum += h1[x];
+            if (ba < 0 && cum >= r_lo) ba = x;
+            if (cum >= r_hi) {
+                bb = x;
+                break;
+            }
+        }
+        if (ba < 0) ba = 255;
+        const float top2 = invw1 > 0.f ? top1 - ((float)ba - 0.5f) / invw1 : top1;
+        const float invw2 = invw1 > 0.f ? invw1 * 256.f / (float)(bb - ba + 1) : 0.f;
+        p.tk_lo[row] = (float)ba;  // stash the level-1 range for stage 3
+        p.tk_hi[row] = (float)bb;
+        p.tk_top[row] = top2;
+        p.tk_invw[row] = invw2;
+        return;
+    }
+    const int ba = (int)p.tk_lo[row], bb = (int)p.tk_hi[row];
+    const uint32_t* h2 = p.tk_hist + (R + row) * 256;
+    const float top2 = p.tk_top[row], invw2 = p.tk_invw[row];
+    // walk the sample from the top: level-1 bins < b, level-2 sub-bins of b, level-1 bins > b;
+    // hi = upper edge of the piece holding rank r_lo, lo = lower edge of the piece holding r_hi
+    float hi = INFINITY, lo = -INFINITY;
+    bool have_hi = r_lo < 1.0, have_lo = false;
+    double cum = 0.0;
+    auto visit = [&](double cnt, float upper, float lower) {
+        if (!have_hi && cum + cnt >= r_lo) {
+            hi = upper;
+            have_hi = true;
+        }
+        if (!have_lo && cum + cnt >= r_hi) {
+            lo = lower;
+            have_lo = true;
+        }
+        cum += cnt;
+    };
+    const bool flat = invw1 <= 0.f;
+    for (int x = 0; x < 256 && !have_lo; ++x) {
+        if (flat) {  // all sampled scores equal: one bin
+            visit((double)h1[x], top1, top1);
+            continue;
+        }
+        const float up1 = top1 - ((float)x - 0.5f) / invw1, dn1 = top1 - ((float)x + 0.5f) / invw1;
+        if (x < ba || x > bb) {
+            visit((double)h1[x], up1, dn1);
+        } else if (x == ba) {
+            // level-1 bins ba..bb as the 256 level-2 sub-bins; level-1 scores of the range that
+            // level 2 rounded out go half to each edge
+            double in1 = 0.0, in2 = 0.0;
+            for (int z = ba; z <= bb; ++z) in1 += h1[z];
+            for (int y = 0; y < 256; ++y) in2 += h2[y];
+            const double rest = in1 > in2 ? in1 - in2 : 0.0;
+            const float dnb = top1 - ((float)bb + 0.5f) / invw1;
+            visit(rest * 0.5, up1, up1);
+            for (int y = 0; y < 256 && !have_lo; ++y)
+                visit((double)h2[y], top2 - ((float)y - 0.5f) / invw2, top2 - ((float)y + 0.5f) / invw2);
+            visit(rest * 0.5, dnb, dnb);
+        }
+    }
+    const float e = 1.0f / 65536.0f;
+    p.tk_hi[row] = hi == INFINITY ? INFINITY : hi + fabsf(hi) * e + 1e-30f;
+    p.tk_lo[row] = lo == -INFINITY ? -INFINITY : lo - fabsf(lo) * e - 1e-30f;
+}
+
+// One warp per row: exact k'-th largest (k' = k - #above) among the window candidates, radix
+// select on order keys (4 x 8-bit digits, warp-private shared histogram).
+__global__ void __launch_bounds__(256) tk_exact_kernel(const __grid_constant__ SelectParams p) {
+    __shared__ uint32_t hist[8][256];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * 8 + wid;
+    if (row >= p.BH * p.Np) return;
+    const int64_t i = row % p.Np;
+    const int64_t vis_real = p.causal ? min(p.N_real, (i + 1) * (int64_t)p.pq) : p.N_real;
+    const int64_t ki = tk_budget(p, vis_real);
+    // candidates: n_seg slices of subcap = cand_cap / n_seg (p.n_seg of the candidate pass)
+    const int64_t subcap = p.cand_cap / p.n_seg;
+    int64_t n = 0;
+    bool over = false;
+    for (int64_t sg = 0; sg < p.n_seg; ++sg) {
+        const int64_t c = p.tk_ncand[row * p.n_seg + sg];
+        n += c;
+        over |= c > subcap;
+    }
+    const int64_t above = p.tk_cabove[row];
+    if (!(above < ki && ki <= above + n && !over)) {
+        if (lane == 0) {
+            p.tk_fail[row] = 1u;
+            atomicAdd(p.tk_nfail, 1);
+        }
+        return;
+    }
+    const float* cand = p.tk_cand + row * p.cand_cap;
+    uint32_t krem = (uint32_t)(ki - above);
+    uint32_t* h = hist[wid];
+    // every candidate lies in [lo, hi]: the leading bytes their order keys share with both
+    // bounds are known, so the radix starts at the first byte where the bounds differ
+    const uint32_t klo = f32_order_key(p.tk_lo[row]), khi = f32_order_key(p.tk_hi[row]);
+    int first = 0;
+    while (first < 3 && (klo >> (24 - 8 * first)) == (khi >> (24 - 8 * first))) ++first;
+    uint32_t prefix = first > 0 ? (klo >> (32 - 8 * first)) : 0u;
+    for (int pass = first; pass < 4; ++pass) {
+        for (int bin = lane; bin < 256; bin += 32) h[bin] = 0u;
+        __syncwarp();
+        const int sh = 24 - 8 * pass;
+        for (int64_t sg = 0; sg < p.n_seg; ++sg) {
+            const int64_t c = p.tk_ncand[row * p.n_seg + sg];
+            const float* cs = cand + sg * subcap;
+            for (int64_t x = lane; x < c; x += 32) {
+                const uint32_t u = f32_order_key(cs[x]);
+                if (pass == 0 || (u >> (sh + 8)) == prefix) atomicAdd(&h[(u >> sh) & 255u], 1u);
+            }
+        }
+        __syncwarp();
+        // from the top: lane l owns bins [255 - 8l - 7, 255 - 8l]
+        uint32_t own = 0;
+        for (int t = 0; t < 8; ++t) own += h[255 - 8 * lane - t];
+        uint32_t incl = own;  // inclusive prefix over lanes (bins from the top)
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t excl = incl - own;
+        const unsigned ball = __ballot_sync(0xffffffffu, incl >= krem);
+        const int L = __ffs(ball) - 1;  // first lane whose bins reach krem
+        uint32_t cum = __shfl_sync(0xffffffffu, excl, L);
+        int bin = 255 - 8 * L;
+        for (int t = 0; t < 8; ++t, --bin) {
+            const uint32_t hc = h[bin];
+            if (cum + hc >= krem) break;
+            cum += hc;
+        }
+        prefix = (prefix << 8) | (uint32_t)bin;
+        krem -= cum;
+        __syncwarp();
+    }
+    if (lane == 0) {
+        p.tk_prefix[row] = prefix;
+        p.tk_krem[row] = krem;
+        p.counts[row] = (unsigned long long)ki;  // top-k keeps exactly k_i keys
+    }
+    // kept candidates -> bitmask (the keys above the window were set by the candidate pass):
+    // key > theta, or == theta while ties remain, lowest index first (R12; candidates are
+    // stored in ascending key order, segment by segment)
+    uint32_t* bm = p.bitmask + row * p.words_per_row;
+    const int32_t* cidx = p.tk_cidx + row * p.cand_cap;
+    uint32_t ties = 0;
+    for (int64_t sg = 0; sg < p.n_seg; ++sg) {
+        const int64_t c = p.tk_ncand[row * p.n_seg + sg];
+        const float* cs = cand + sg * subcap;
+        const int32_t* is = cidx + sg * subcap;
+        for (int64_t x0 = 0; x0 < c; x0 += 32) {
+            const int64_t x = x0 + lane;
+            const bool valid = x < c;
+            const uint32_t u = valid ? f32_order_key(cs[x]) : 0u;
+            const bool tie = valid && u == prefix;
+            const unsigned tb = __ballot_sync(0xffffffffu, tie);
+            const uint32_t rank = ties + __popc(tb & ((1u << lane) - 1u));
+            const bool keep = valid && (u > prefix || (tie && rank < krem));
+            if (keep) {
+                const int32_t key = is[x];
+                atomicOr(&bm[key >> 5], 1u << (key & 31));
+            }
+            ties += __popc(tb);
+        }
+    }
+}
+
+cudaError_t launch_tk_sample_k(const void* k, void* ks, int64_t BHkv, int64_t N, int64_t Ns, int64_t D, int stride,
+                               cudaStream_t st) {
+    const int64_t total = BHkv * Ns * (D / 8);
+    if (total <= 0) return cudaSuccess;
+    const int64_t nb = (total + 255) / 256;
+    const int grid = (int)(nb < 148 * 16 ? nb : 148 * 16);
+    tk_sample_k_kernel<<<grid, 256, 0, st>>>(static_cast<const uint4*>(k), static_cast<uint4*>(ks), BHkv, N, Ns, D,
+                                             stride);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tk_rows(const SelectParams& p, int stage, int stride, cudaStream_t st) {
+    const int64_t R = p.BH * p.Np;
+    if (R <= 0) return cudaSuccess;
+    tk_rows_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(p, stage, stride);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tk_exact(const SelectParams& p, cudaStream_t st) {
+    const int64_t R = p.BH * p.Np;
+    if (R <= 0) return cudaSuccess;
+    tk_exact_kernel<<<(unsigned)((R + 7) / 8), 256, 0, st>>>(p);
     return cudaGetLastError();
 }
 

@@ -1,11 +1,22 @@
+"""Per-kernel time of one TOPK selection at dit128k (24 heads, keep 21.5%), via torch.profiler."""
 import os, sys, torch
-sys.path.insert(0, os.getcwd())
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench
 from paper_2603_29494_b200 import synth
 import paper_2603_29494_b200.vecattn as va
+from torch.profiler import ProfilerActivity, profile
+H = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 wl = synth.WORKLOADS["dit128k"]
-q, k, v = bench.build_inputs(wl, "video", torch.device("cuda"), 0, 4)
+q, k, v = bench.build_inputs(wl, "video", torch.device("cuda"), 0, H)
 cfg = va.SelectConfig(mode="topk", pq=64, keep_frac=0.215)
 off, idx = va.select(q, k, cfg)
 torch.cuda.synchronize()
-print("nnz", int(off[-1]))
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    off, idx = va.select(q, k, cfg)
+    torch.cuda.synchronize()
+tot = 0.0
+for e in prof.events():
+    if e.device_type.name == "CUDA":
+        print(f"{e.device_time_total / 1000:9.3f} ms  {e.name[:110]}")
+        tot += e.device_time_total / 1000
+print(f"total {tot:.3f} ms, nnz {int(off[-1])}")
