@@ -163,7 +163,7 @@ SelectWs carve_select(const vecattn_problem_t* p, int32_t pq, void* base, bool t
             off += align_up((size_t)R * 4);
         }
         w.tk_ncand = reinterpret_cast<uint32_t*>(b + off);  // [R][candidate-pass segments]
-        off += align_up((size_t)R * 4 * (size_t)((p->N + kTkCandSeg - 1) / kTkCandSeg));
+        off += align_up((size_t)R * 4 * 2 * (size_t)((p->N + kTkCandSeg - 1) / kTkCandSeg));  // x 2 warp sets
         float** f32s[] = {&w.tk_top, &w.tk_invw, &w.tk_lo, &w.tk_hi};
         for (float** x : f32s) {
             *x = reinterpret_cast<float*>(b + off);
@@ -370,7 +370,7 @@ cudaError_t run_select(const vecattn_problem_t* p, const vecattn_select_params_t
                 sp.cand_cap = cap_keep;
                 if (e == cudaSuccess && getenv("VECATTN_TOPK_DEBUG")) {  // diagnostics (scripts only)
                     cudaStreamSynchronize(cs);
-                    const int64_t nsg = (p->N + kTkCandSeg - 1) / kTkCandSeg;
+                    const int64_t nsg = 2 * ((p->N + kTkCandSeg - 1) / kTkCandSeg);
                     std::vector<uint32_t> ab(R), nc(R), fl(R), ncs(R * nsg);
                     std::vector<float> lo(R), hi(R);
                     int nf = 0;

@@ -37,7 +37,7 @@ namespace {
 // the TOPK histogram passes, whose two warp sets take alternate 64-key chunks of every tile
 // and update the same per-row histogram with shared-memory atomics.
 template <int EPI>
-constexpr int epi_warps() { return (EPI == EPI_TOPK_HIST || EPI == EPI_TK_SHIST) ? 8 : 4; }
+constexpr int epi_warps() { return (EPI == EPI_TOPK_HIST || EPI == EPI_TK_SHIST || EPI == EPI_TK_CAND) ? 8 : 4; }
 template <int EPI>
 constexpr int sel_threads() { return 64 + 32 * epi_warps<EPI>(); }
 
@@ -47,7 +47,7 @@ struct SelCfg {
     static constexpr int kQBytes = kCB * 128 * 128;          // Q_p tile
     static constexpr int kKStageBytes = kCB * BN * 128;      // one K tile
     static constexpr int kHistBytes = (EPI == EPI_TOPK_HIST || EPI == EPI_TK_SHIST) ? 256 * 128 * 4
-                                      : (EPI == EPI_TK_CAND ? 64 * 128 * 4 : 0);  // CAND: score staging
+                                      : (EPI == EPI_TK_CAND ? 2 * 64 * 128 * 4 : 0);  // CAND: score staging per warp set
     static constexpr int kOffQ = 0;
     static constexpr int kOffK = kQBytes;
     static constexpr int kOffHist = kOffK + STAGES * kKStageBytes;
@@ -214,9 +214,11 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
             }
         }
         // CAND: this (row, key segment)'s candidate slice; subcap = cand_cap / n_seg
-        const int64_t subcap = (EPI == EPI_TK_CAND) ? p.cand_cap / p.n_seg : 0;
-        float* cand_row = (EPI == EPI_TK_CAND) ? p.tk_cand + grow * p.cand_cap + seg * subcap : nullptr;
-        int32_t* cidx_row = (EPI == EPI_TK_CAND) ? p.tk_cidx + grow * p.cand_cap + seg * subcap : nullptr;
+        // (two warp sets: slice (seg, set) of cand_cap / (2 n_seg) entries per row)
+        const int64_t subcap = (EPI == EPI_TK_CAND) ? p.cand_cap / (2 * p.n_seg) : 0;
+        const int64_t slice = 2 * seg + eset;
+        float* cand_row = (EPI == EPI_TK_CAND) ? p.tk_cand + grow * p.cand_cap + slice * subcap : nullptr;
+        int32_t* cidx_row = (EPI == EPI_TK_CAND) ? p.tk_cidx + grow * p.cand_cap + slice * subcap : nullptr;
         uint32_t tk_prefix = 0, tk_krem = 0, tk_taken = 0;
         unsigned long long cnt = 0;
         uint32_t* hist = reinterpret_cast<uint32_t*>(smem + C::kOffHist);
@@ -431,7 +433,7 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
                     // extraction: the 64 scores go to a column-major shared stage (conflict-free:
                     // lanes are consecutive rows), then each thread walks its set bits (~4% of
                     // scores) reading the stage with a dynamic index
-                    float* stg = reinterpret_cast<float*>(hist) + r;
+                    float* stg = reinterpret_cast<float*>(hist) + eset * 64 * 128 + r;
                     if ((in0 | in1) != 0u) {
 #pragma unroll
                         for (int j = 0; j < 64; ++j) stg[j * 128] = v[j];
@@ -511,7 +513,10 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
             mbar_arrive(&acc_empty[buf]);
 
             if constexpr (EPI == EPI_ALG1 || EPI == EPI_THRESH || EPI == EPI_TOPK_EMIT || EPI == EPI_TK_CAND) {
-                if (row_ok) {
+                if (row_ok && epi_warps<EPI>() == 8) {  // CAND, two warp sets: each stores its 64-key chunk's words
+                    uint32_t* dst = p.bitmask + grow * p.words_per_row + key0 / 32 + 2 * eset;
+                    *reinterpret_cast<uint2*>(dst) = make_uint2(words[2 * eset], words[2 * eset + 1]);
+                } else if (row_ok) {
                     uint32_t* dst = p.bitmask + grow * p.words_per_row + key0 / 32;
 #pragma unroll
                     for (int w = 0; w < BN / 32; w += 4) {
@@ -537,7 +542,7 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
                 }
             } else if constexpr (EPI == EPI_TK_CAND) {
                 if (above) atomicAdd(&p.tk_cabove[grow], above);
-                p.tk_ncand[grow * p.n_seg + seg] = ncand;
+                p.tk_ncand[grow * 2 * p.n_seg + slice] = ncand;
             } else if constexpr (EPI == EPI_TK_SHIST) {
                 uint32_t* gh = p.tk_hist + ((int64_t)p.pass * p.BH * p.Np + grow) * 256;
                 if (p.n_seg == 1) {  // the whole sampled row in this unit: plain 16-B stores, half per warp set
@@ -794,21 +799,25 @@ __global__ void __launch_bounds__(256) tk_rows_kernel(const __grid_constant__ Se
 }
 
 // One warp per row: exact k'-th largest (k' = k - #above) among the window candidates, radix
-// select on order keys (4 x 8-bit digits, warp-private shared histogram).
+// select on order keys (4 x 8-bit digits, warp-private shared histogram), then the kept
+// candidates' bits: key > theta, and the k_rem lowest-index keys == theta (R12).  Candidates
+// are in slices (candidate-pass segment x warp set), so ties are ranked by index explicitly.
+constexpr int kTkMaxTies = 1024;
 __global__ void __launch_bounds__(256) tk_exact_kernel(const __grid_constant__ SelectParams p) {
     __shared__ uint32_t hist[8][256];
+    __shared__ int32_t tie_idx[8][kTkMaxTies];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t row = (int64_t)blockIdx.x * 8 + wid;
     if (row >= p.BH * p.Np) return;
     const int64_t i = row % p.Np;
     const int64_t vis_real = p.causal ? min(p.N_real, (i + 1) * (int64_t)p.pq) : p.N_real;
     const int64_t ki = tk_budget(p, vis_real);
-    // candidates: n_seg slices of subcap = cand_cap / n_seg (p.n_seg of the candidate pass)
-    const int64_t subcap = p.cand_cap / p.n_seg;
+    const int64_t nsl = 2 * p.n_seg;  // slices
+    const int64_t subcap = p.cand_cap / nsl;
     int64_t n = 0;
     bool over = false;
-    for (int64_t sg = 0; sg < p.n_seg; ++sg) {
-        const int64_t c = p.tk_ncand[row * p.n_seg + sg];
+    for (int64_t sg = 0; sg < nsl; ++sg) {
+        const int64_t c = p.tk_ncand[row * nsl + sg];
         n += c;
         over |= c > subcap;
     }
@@ -821,6 +830,7 @@ __global__ void __launch_bounds__(256) tk_exact_kernel(const __grid_constant__ S
         return;
     }
     const float* cand = p.tk_cand + row * p.cand_cap;
+    const int32_t* cidx = p.tk_cidx + row * p.cand_cap;
     uint32_t krem = (uint32_t)(ki - above);
     uint32_t* h = hist[wid];
     // every candidate lies in [lo, hi]: the leading bytes their order keys share with both
@@ -833,8 +843,8 @@ __global__ void __launch_bounds__(256) tk_exact_kernel(const __grid_constant__ S
         for (int bin = lane; bin < 256; bin += 32) h[bin] = 0u;
         __syncwarp();
         const int sh = 24 - 8 * pass;
-        for (int64_t sg = 0; sg < p.n_seg; ++sg) {
-            const int64_t c = p.tk_ncand[row * p.n_seg + sg];
+        for (int64_t sg = 0; sg < nsl; ++sg) {
+            const int64_t c = p.tk_ncand[row * nsl + sg];
             const float* cs = cand + sg * subcap;
             for (int64_t x = lane; x < c; x += 32) {
                 const uint32_t u = f32_order_key(cs[x]);
@@ -864,35 +874,54 @@ __global__ void __launch_bounds__(256) tk_exact_kernel(const __grid_constant__ S
         krem -= cum;
         __syncwarp();
     }
-    if (lane == 0) {
-        p.tk_prefix[row] = prefix;
-        p.tk_krem[row] = krem;
-        p.counts[row] = (unsigned long long)ki;  // top-k keeps exactly k_i keys
-    }
-    // kept candidates -> bitmask (the keys above the window were set by the candidate pass):
-    // key > theta, or == theta while ties remain, lowest index first (R12; candidates are
-    // stored in ascending key order, segment by segment)
+    // kept candidates -> bitmask (the keys above the window were set by the candidate pass);
+    // ties (key == theta) are gathered and the krem lowest indices kept
     uint32_t* bm = p.bitmask + row * p.words_per_row;
-    const int32_t* cidx = p.tk_cidx + row * p.cand_cap;
-    uint32_t ties = 0;
-    for (int64_t sg = 0; sg < p.n_seg; ++sg) {
-        const int64_t c = p.tk_ncand[row * p.n_seg + sg];
+    int32_t* tl = tie_idx[wid];
+    uint32_t nt = 0;
+    for (int64_t sg = 0; sg < nsl; ++sg) {
+        const int64_t c = p.tk_ncand[row * nsl + sg];
         const float* cs = cand + sg * subcap;
         const int32_t* is = cidx + sg * subcap;
         for (int64_t x0 = 0; x0 < c; x0 += 32) {
             const int64_t x = x0 + lane;
-            const bool valid = x < c;
-            const uint32_t u = valid ? f32_order_key(cs[x]) : 0u;
-            const bool tie = valid && u == prefix;
-            const unsigned tb = __ballot_sync(0xffffffffu, tie);
-            const uint32_t rank = ties + __popc(tb & ((1u << lane) - 1u));
-            const bool keep = valid && (u > prefix || (tie && rank < krem));
-            if (keep) {
+            const uint32_t u = x < c ? f32_order_key(cs[x]) : 0u;
+            const bool gt = x < c && u > prefix, tie = x < c && u == prefix;
+            if (gt) {
                 const int32_t key = is[x];
                 atomicOr(&bm[key >> 5], 1u << (key & 31));
             }
-            ties += __popc(tb);
+            const unsigned tb = __ballot_sync(0xffffffffu, tie);
+            if (tie) {
+                const uint32_t slot = nt + __popc(tb & ((1u << lane) - 1u));
+                if (slot < kTkMaxTies) tl[slot] = is[x];
+            }
+            nt += __popc(tb);
         }
+    }
+    __syncwarp();
+    if (nt > kTkMaxTies) {  // too many ties to rank here: radix fallback for this row
+        if (lane == 0) {
+            p.tk_fail[row] = 1u;
+            atomicAdd(p.tk_nfail, 1);
+        }
+        return;
+    }
+    if (nt == krem) {
+        for (uint32_t t = lane; t < nt; t += 32) atomicOr(&bm[tl[t] >> 5], 1u << (tl[t] & 31));
+    } else {
+        // rank of each tie by index among the ties (indices are distinct)
+        for (uint32_t t = lane; t < nt; t += 32) {
+            const int32_t a = tl[t];
+            uint32_t rank = 0;
+            for (uint32_t o = 0; o < nt; ++o) rank += tl[o] < a ? 1u : 0u;
+            if (rank < krem) atomicOr(&bm[a >> 5], 1u << (a & 31));
+        }
+    }
+    if (lane == 0) {
+        p.tk_prefix[row] = prefix;
+        p.tk_krem[row] = krem;
+        p.counts[row] = (unsigned long long)ki;  // top-k keeps exactly k_i keys
     }
 }
 
