@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             int item = 0;
             if (lane == 0) {
                 if (it >= 2) mbar_wait(&bars[C::B_IEMPTY + slot], ((it >> 1) - 1) & 1);
-                item = atomicAdd(p.work_counter, 1);
+                item = plan::next_item(p);
                 item_slot[slot] = item < p.total_items ? item : -1;
                 mbar_arrive(&bars[C::B_IFULL + slot]);
             }

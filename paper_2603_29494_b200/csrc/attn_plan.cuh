@@ -28,6 +28,25 @@ VA_DEV void trace(const AttnParams& p, int kind, int64_t c) {
         p.trace[(int64_t)(kind + 16 * blockIdx.x) * kTraceChunks + c] = globaltimer_ns();
 }
 
+// Dynamic item scheduler.  die_mode 0: one atomic counter over the head-major item order.
+// die_mode 1/2: one counter per die of the GPU (two L2 halves); die d walks the heads
+// h = d, d+2, ... so each die's L2 holds the K/V of fewer heads, and takes the other die's
+// items once its own are gone.  Returns an item index >= total_items when all are done.
+VA_DEV int next_item(const AttnParams& p) {
+    if (p.die_mode == 0) return atomicAdd(p.work_counter, 1);
+    uint32_t smid, nsm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    asm volatile("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+    const int d0 = p.die_mode == 1 ? (smid >= nsm / 2 ? 1 : 0) : (int)(smid & 1u);
+    for (int t = 0; t < 2; ++t) {
+        const int d = d0 ^ t;
+        const int li = atomicAdd(p.work_counter + d, 1);
+        const int64_t head = 2 * (li / p.n_mt) + d;
+        if (head < p.BH) return (int)(head * p.n_mt + li % p.n_mt);
+    }
+    return (int)p.total_items;
+}
+
 struct Item {
     int64_t bh, it;  // head, 256-row item within the head
     int n_chunks;

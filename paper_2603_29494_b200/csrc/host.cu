@@ -816,6 +816,10 @@ static vecattn_status_t attn_common(const vecattn_problem_t* p, const void* q, c
     ap.causal = p->causal ? 1 : 0;
     ap.scale = scale;
     ap.scale_log2 = scale * 1.4426950408889634f;
+    {
+        const char* dm = getenv("VECATTN_DIE_SPLIT");
+        ap.die_mode = dm ? atoi(dm) : 0;
+    }
     {   // debug timeline: VECATTN_TRACE=<device pointer as decimal> (tests/scripts only)
         const char* tr = getenv("VECATTN_TRACE");
         ap.trace = tr ? reinterpret_cast<long long*>(strtoull(tr, nullptr, 10)) : nullptr;
@@ -864,7 +868,7 @@ vecattn_status_t vecattn_sparse_fwd(const vecattn_problem_t* p, int32_t pq, cons
     tmark(1, cs);
     cudaError_t e = va::launch_worklist(offsets, indices ? indices : reinterpret_cast<const int32_t*>(wl), wl, wl_len,
                                         ap->BH, ap->Np, ap->n_mt, p->N, pq, nnz_cap, cs);
-    if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, sizeof(int), cs);
+    if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, 2 * sizeof(int), cs);
     tmark(2, cs);
     if (e == cudaSuccess) e = va::launch_attn(*ap, (int)p->D, true, attn_grid(ap->total_items), cs);
     tmark(3, cs);
@@ -895,7 +899,7 @@ vecattn_status_t vecattn_dense_fwd(const vecattn_problem_t* p, const void* q, co
     ap->Np = (p->N + 127) / 128;
     ap->pq = 128;
     ap->work_counter = reinterpret_cast<int*>(ws);
-    cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(int), cs);
+    cudaError_t e = cudaMemsetAsync(ws, 0, 2 * sizeof(int), cs);
     if (g_timing.enabled) tbegin(false, false);
     tmark(2, cs);
     if (e == cudaSuccess) e = va::launch_attn(*ap, (int)p->D, false, attn_grid(ap->total_items), cs);
@@ -985,7 +989,7 @@ vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_selec
     if (e == cudaSuccess)
         e = va::launch_plan(w.bitmask, sp->words_per_row, offsets, d_nnz, nnz_cap, wl, wl_len, sp->BH, sp->Np, p->N,
                             s->pq, p->causal ? 1 : 0, cs);
-    if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, sizeof(int), cs);
+    if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, 2 * sizeof(int), cs);
     tmark(2, cs);
     std::unique_lock<std::mutex> lk;
     if (e == cudaSuccess && side) {
