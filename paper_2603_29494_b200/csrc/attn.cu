@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     sMeta[s * kChunk + kb + 32 + lane] = ok1 ? key1 : kPad;
                     __syncwarp();
                     if (lane == 0) {
-                        mbar_arrive(&bars[C::B_MFULL + s]);
+                        if (p.causal) mbar_arrive(&bars[C::B_MFULL + s]);  // waited by the causal softmax only
                         mbar_arrive_expect_tx(&bars[C::B_VFULL + s], 64 * D * 2);
                     }
                     if (lane < 16) {

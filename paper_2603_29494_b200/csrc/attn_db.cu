@@ -276,7 +276,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                     sMeta[s * kChunk + 32 + lane] = ok1 ? key1 : kPad;
                     __syncwarp();
                     if (lane == 0) {
-                        mbar_arrive(&bars[C::B_MFULL + s]);
+                        // the causal-key hand-off has a waiter only in the causal softmax (an
+                        // unobserved arrive is what compute-sanitizer synccheck flags)
+                        if (p.causal) mbar_arrive(&bars[C::B_MFULL + s]);
                         mbar_arrive_expect_tx(&bars[C::B_VFULL + s], kChunk * D * 2);
                     }
                     if (lane < 16) {
@@ -517,7 +519,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                 // SFULL(ct) fired, so every MMA issued before S(ct) -- including PV(ct-2) of
                 // this tile -- is complete: ODONE phases 0..ct-2 are done (parity waits on
                 // phase ct-1 are then unambiguous).
-                if (ct >= 1 && od < ct - 1) od = ct - 1;
+                // Default: the phases are only counted (od), never waited on unless a rescale needs
+                // PV(ct-1).  p.strict_sync (VECATTN_STRICT_SYNC=1): every ODONE phase is waited on
+                // before the next commit can arrive, which compute-sanitizer synccheck requires (it
+                // reports an unobserved mbarrier phase as "missing wait"); ~2% slower at dit128k.
+                if (p.strict_sync) {
+                    for (; od + 1 < ct; ++od) mbar_wait(&bars[C::B_ODONE + tile], od & 1u);
+                } else if (ct >= 1 && od < ct - 1) {
+                    od = ct - 1;
+                }
                 const bool need = m_new > m_ref + 8.0f;
                 const float corr = need ? ex2(m_ref - m_new) : 1.0f;
                 if (need) {
@@ -560,6 +570,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                     tmem_st32(tS, pk);
                     tmem_st_wait();
                 }
+                if (p.strict_sync)  // PV(ct-1)'s phase, observed before PV(ct) (needs P(ct)) can commit
+                    for (; od < ct; ++od) mbar_wait(&bars[C::B_ODONE + tile], od & 1u);
                 tc_fence_before();
                 mbar_arrive(&bars[C::B_PFULL + 2 * tile + bi]);
                 if (lane == 0 && (warp == 2 || warp == 6)) trace(p, 7 + 2 * tile, c);

@@ -819,6 +819,7 @@ static vecattn_status_t attn_common(const vecattn_problem_t* p, const void* q, c
     {
         const char* dm = getenv("VECATTN_DIE_SPLIT");
         ap.die_mode = dm ? atoi(dm) : 0;
+        ap.strict_sync = getenv("VECATTN_STRICT_SYNC") ? 1 : 0;
     }
     {   // debug timeline: VECATTN_TRACE=<device pointer as decimal> (tests/scripts only)
         const char* tr = getenv("VECATTN_TRACE");

@@ -142,6 +142,7 @@ struct AttnParams {
     int64_t N, Np, BH, Hq, Hkv, n_mt /* 256-row items per head */, total_items;
     int32_t pq, causal;
     float scale, scale_log2;
+    int32_t strict_sync;           // attn_db: wait on every ODONE phase (compute-sanitizer synccheck runs)
     int32_t die_mode;              // item scheduler: 0 one counter (head-major); 1/2 one counter per die
                                    // (die = smid < nsmid/2 / smid & 1), die d takes heads h = d (mod 2)
 };
