@@ -21,7 +21,7 @@ if os.path.exists(lf):
     ours = {k: v for k, v in agg.items() if "va::" in k or "attn_" in k or "select_kernel" in k}
     lines += ["## Launch list (gpu__time_duration.sum, --clock-control none; cold-cache, serialised)", "",
               "Source command: `ncu --metrics gpu__time_duration.sum --clock-control none --csv "
-              "python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --alpha 1.0039 --dense-reps 1`", "",
+              "python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --alpha 1.0039 --dense-reps 1 --no-context --no-causal-extra`", "",
               "| kernel | launches | mean ms | total ms |", "|---|---|---|---|"]
     for k, v in sorted(ours.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"| `{k[:70]}` | {len(v)} | {sum(v)/len(v):.3f} | {sum(v):.2f} |")
