@@ -53,24 +53,34 @@ constexpr uint32_t kPad = 0x0FFFFFFFu;      // meta key for padding lanes (sorts
 
 template <int D>
 struct AttnCfg {
-    static constexpr int kStages = D == 128 ? 4 : 8;
+    static constexpr int kStages = D == 128 ? 4 : 8;   // K ring (and Q_ext/K_ext bias rows)
+#ifndef VA_DB_VSTAGES
+#define VA_DB_VSTAGES 4
+#endif
+    // V ring depth (build knob): a chunk's V gathers are issued after its K gathers and its
+    // stage frees only when PV(c - VS) completes, so V lands just in time for PV (%globaltimer
+    // trace: PV waits ~0.8 us per chunk on V).  VS = 5 fits in shared memory but is slower in
+    // the full step (attention 76.8 vs 74.4 ms, A/B in one box run): the remaining L1 shrinks,
+    // and the side-stream CSR emission no longer fits beside the attention CTA.
+    static constexpr int kVStages = D == 128 ? VA_DB_VSTAGES : 8;
     static constexpr int kCB = D / 64;
     static constexpr int kQTileBytes = kCB * 128 * 128;   // 128 rows x D bf16
     static constexpr int kKVBytes = kCB * kChunk * 128;    // 64 keys x D bf16
     static constexpr int kOffQ = 0;                        // two Q tiles
     static constexpr int kOffK = 2 * kQTileBytes;
     static constexpr int kOffV = kOffK + kStages * kKVBytes;
-    static constexpr int kOffMeta = kOffV + kStages * kKVBytes;
-    static constexpr int kOffQx = (kOffMeta + kStages * kChunk * 4 + 1023) / 1024 * 1024;  // Q_ext [2][128 x 16]
+    static constexpr int kOffMeta = kOffV + kVStages * kKVBytes;
+    static constexpr int kOffQx = (kOffMeta + kVStages * kChunk * 4 + 1023) / 1024 * 1024;  // Q_ext [2][128 x 16]
     static constexpr int kOffKx = kOffQx + 2 * 128 * 16 * 2;                               // K_ext [S][64 x 16]
     static constexpr int kOffBar = kOffKx + kStages * kChunk * 16 * 2;
     static constexpr int B_QFULL = 0, B_QEMPTY = 1, B_KFULL = 2, B_KEMPTY = B_KFULL + kStages,
-                         B_VFULL = B_KEMPTY + kStages, B_VEMPTY = B_VFULL + kStages,
-                         B_MFULL = B_VEMPTY + kStages, B_SFULL = B_MFULL + kStages /* [2 tiles][2 bufs] */,
+                         B_VFULL = B_KEMPTY + kStages, B_VEMPTY = B_VFULL + kVStages,
+                         B_MFULL = B_VEMPTY + kVStages, B_SFULL = B_MFULL + kVStages /* [2 tiles][2 bufs] */,
                          B_PFULL = B_SFULL + 4, B_ODONE = B_PFULL + 4, B_OEMPTY = B_ODONE + 2,
                          B_IFULL = B_OEMPTY + 2, B_IEMPTY = B_IFULL + 2, B_OFIN = B_IEMPTY + 2, kNumBars = B_OFIN + 2;
     static constexpr int kOffItem = kOffBar + kNumBars * 8;
     static constexpr int kSmem = kOffItem + 16;
+    static_assert(kSmem <= 227 * 1024, "shared memory");
     // TMEM: O_t at 128t (D cols); S[t][b] at 256 + 128t + 64b (64 cols; P over its first 32)
     static constexpr uint32_t kTmemCols = 512;
     static constexpr uint32_t kIdescS = make_idesc_bf16(128, kChunk, 0, 0);
@@ -95,6 +105,7 @@ template <int D, bool GATHER>
 __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_constant__ AttnParams p) {
     using C = AttnCfg<D>;
     constexpr int S_ = C::kStages;
+    constexpr int VS = C::kVStages;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sQ = smem + C::kOffQ;
     uint8_t* sK = smem + C::kOffK;
@@ -115,6 +126,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
         for (int s = 0; s < S_; ++s) {
             mbar_init(&bars[C::B_KFULL + s], 1);
             mbar_init(&bars[C::B_KEMPTY + s], 1);
+        }
+        for (int s = 0; s < VS; ++s) {
             mbar_init(&bars[C::B_VFULL + s], 1);
             mbar_init(&bars[C::B_VEMPTY + s], 1);
             mbar_init(&bars[C::B_MFULL + s], 1);
@@ -198,8 +211,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
         // ahead), lanes 0-15 issue the tile::gather4s; K_ext bias rows are written before the
         // K gathers (consumed by the S MMA, freed with KEMPTY), the keys for the causal mask
         // before the V gathers (freed with VEMPTY).
-        static_assert(S_ % kLoadWarps == 0, "stage ownership");
-        const int g = (int)warp - kFirstLoadWarp;
+        // VA_DB_KV_SPLIT: warps 0-1 load only K (chunks c = g mod 2), warps 2-3 only V, so a
+        // chunk's V gathers do not queue behind its K gathers in one warp.
+#ifndef VA_DB_KV_SPLIT
+#define VA_DB_KV_SPLIT 0
+#endif
+        constexpr bool kSplit = VA_DB_KV_SPLIT != 0;
+        constexpr int NW = kSplit ? kLoadWarps / 2 : kLoadWarps;  // warps per role
+        static_assert(S_ % NW == 0, "stage ownership");
+        const int g0 = (int)warp - kFirstLoadWarp;
+        const bool k_role = !kSplit || g0 < NW, v_role = !kSplit || g0 >= NW;
+        const int g = kSplit ? g0 % NW : g0;
         int64_t c = 0;  // chunks of all previous items
         for (int it = 0;; ++it) {
             const int slot = it & 1;
@@ -212,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
             if (I.n_chunks == 0) continue;
             const int64_t b = I.bh / p.Hq, h = I.bh % p.Hq;
             const int64_t bh_kv = b * p.Hkv + h / (p.Hq / p.Hkv);
-            int j = (int)(((int64_t)g - c % kLoadWarps + kLoadWarps) % kLoadWarps);  // first owned chunk
+            int j = (int)(((int64_t)g - c % NW + NW) % NW);  // first owned chunk
             if constexpr (GATHER) {
                 const uint32_t* wlp = p.wl + I.base;
                 Chunk ch;
@@ -221,14 +243,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                 if (j < I.n_chunks) ch = chunk_info<true>(I, j);
                 uint32_t e0 = (int)lane < ch.len ? __ldcs(wlp + ch.start + lane) : 0u;
                 uint32_t e1 = 32 + (int)lane < ch.len ? __ldcs(wlp + ch.start + 32 + lane) : 0u;
-                for (; j < I.n_chunks; j += kLoadWarps) {
+                for (; j < I.n_chunks; j += NW) {
                     const int64_t cc = c + j;
                     const int s = (int)(cc % S_);
                     const int round = (int)(cc / S_);
                     Chunk chn;
                     chn.len = 0;
                     chn.start = 0;
-                    if (j + kLoadWarps < I.n_chunks) chn = chunk_info<true>(I, j + kLoadWarps);
+                    if (j + NW < I.n_chunks) chn = chunk_info<true>(I, j + NW);
                     const uint32_t en0 = (int)lane < chn.len ? __ldcs(wlp + chn.start + lane) : 0u;
                     const uint32_t en1 = 32 + (int)lane < chn.len ? __ldcs(wlp + chn.start + 32 + lane) : 0u;
                     const bool ok0 = (int)lane < ch.len, ok1 = 32 + (int)lane < ch.len;
@@ -243,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                     const bool lo = lane < 8;
                     const int ra = lo ? a0 : b0_, rb = lo ? a1 : b1_, rc = lo ? a2 : b2_, rd = lo ? a3 : b3_;
                     // ---- K: bias rows, then the gathers
+                    if (k_role) {
                     if (lane == 0 && round > 0) mbar_wait(&bars[C::B_KEMPTY + s], (round - 1) & 1);
                     if (lane == 0) trace(p, 0, cc);
                     __syncwarp();
@@ -268,32 +291,39 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                             tma_gather4(dst + cb * kChunk * 128, &p.tm_k, &bars[C::B_KFULL + s], cb * 64, ra, rb, rc,
                                         rd);
                     }
-                    // ---- V: keys for the causal mask, then the gathers
-                    if (lane == 0 && round > 0) mbar_wait(&bars[C::B_VEMPTY + s], (round - 1) & 1);
+                    }
+                    // ---- V: keys for the causal mask, then the gathers.  V stage sv = cc % VS
+                    // is not owned by one warp (VS % 4 != 0), but the wait stays unambiguous:
+                    // this warp's previous V wait (chunk cc - 4) proved PV(cc - 4 - VS) done, so
+                    // PV(cc - 2 VS) -- the phase before the one waited for -- is complete.
+                    if (v_role) {
+                    const int sv = (int)(cc % VS), vround = (int)(cc / VS);
+                    if (lane == 0 && vround > 0) mbar_wait(&bars[C::B_VEMPTY + sv], (vround - 1) & 1);
                     if (lane == 0) trace(p, 1, cc);
                     __syncwarp();
-                    sMeta[s * kChunk + lane] = ok0 ? key0 : kPad;
-                    sMeta[s * kChunk + 32 + lane] = ok1 ? key1 : kPad;
+                    sMeta[sv * kChunk + lane] = ok0 ? key0 : kPad;
+                    sMeta[sv * kChunk + 32 + lane] = ok1 ? key1 : kPad;
                     __syncwarp();
                     if (lane == 0) {
                         // the causal-key hand-off has a waiter only in the causal softmax (an
                         // unobserved arrive is what compute-sanitizer synccheck flags)
-                        if (p.causal) mbar_arrive(&bars[C::B_MFULL + s]);
-                        mbar_arrive_expect_tx(&bars[C::B_VFULL + s], kChunk * D * 2);
+                        if (p.causal) mbar_arrive(&bars[C::B_MFULL + sv]);
+                        mbar_arrive_expect_tx(&bars[C::B_VFULL + sv], kChunk * D * 2);
                     }
                     if (lane < 16) {
-                        uint8_t* dst = sV + s * C::kKVBytes + 4 * (int)lane * 128;
+                        uint8_t* dst = sV + sv * C::kKVBytes + 4 * (int)lane * 128;
 #pragma unroll
                         for (int cb = 0; cb < C::kCB; ++cb)
-                            tma_gather4(dst + cb * kChunk * 128, &p.tm_v, &bars[C::B_VFULL + s], cb * 64, ra, rb, rc,
+                            tma_gather4(dst + cb * kChunk * 128, &p.tm_v, &bars[C::B_VFULL + sv], cb * 64, ra, rb, rc,
                                         rd);
+                    }
                     }
                     e0 = en0;
                     e1 = en1;
                     ch = chn;
                 }
             } else {
-                if (lane == 0) {
+                if (lane == 0 && !kSplit) {
                     for (; j < I.n_chunks; j += kLoadWarps) {
                         const int64_t cc = c + j;
                         const int s = (int)(cc % S_);
@@ -304,11 +334,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                         for (int cb = 0; cb < C::kCB; ++cb)
                             tma_load_3d(sK + s * C::kKVBytes + cb * kChunk * 128, &p.tm_k, &bars[C::B_KFULL + s],
                                         cb * 64, j * kChunk, (int)bh_kv);
-                        if (round > 0) mbar_wait(&bars[C::B_VEMPTY + s], (round - 1) & 1);
-                        mbar_arrive_expect_tx(&bars[C::B_VFULL + s], C::kKVBytes);
+                        const int sv = (int)(cc % VS), vround = (int)(cc / VS);
+                        if (vround > 0) mbar_wait(&bars[C::B_VEMPTY + sv], (vround - 1) & 1);
+                        mbar_arrive_expect_tx(&bars[C::B_VFULL + sv], C::kKVBytes);
 #pragma unroll
                         for (int cb = 0; cb < C::kCB; ++cb)
-                            tma_load_3d(sV + s * C::kKVBytes + cb * kChunk * 128, &p.tm_v, &bars[C::B_VFULL + s],
+                            tma_load_3d(sV + sv * C::kKVBytes + cb * kChunk * 128, &p.tm_v, &bars[C::B_VFULL + sv],
                                         cb * 64, j * kChunk, (int)bh_kv);
                     }
                 }
@@ -352,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                 ++ns[t];
             };
             auto issue_pv = [&](int t, int64_t cc, bool first) {
-                const int s = (int)(cc % S_);
+                const int s = (int)(cc % VS);
                 const int bi = (int)(np_[t] & 1u);
                 mbar_wait(&bars[C::B_PFULL + 2 * t + bi], (np_[t] >> 1) & 1u);
                 ++np_[t];
@@ -412,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                             issue_next_s();
                         }
                     }
-                    mbar_wait(&bars[C::B_VFULL + s], (uint32_t)((c / S_) & 1));
+                    mbar_wait(&bars[C::B_VFULL + (int)(c % VS)], (uint32_t)((c / VS) & 1));
                     trace(p, 3, c);
 #pragma unroll
                     for (int t = 0; t < 2; ++t) {
@@ -421,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                         started[t] = true;
                         trace(p, 4 + t, c);
                     }
-                    mma_commit(&bars[C::B_VEMPTY + s]);
+                    mma_commit(&bars[C::B_VEMPTY + (int)(c % VS)]);
                     if (more && !s_first) {
                         wait_k(c + 1);
                         issue_next_s();
@@ -468,8 +499,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                 if constexpr (GATHER) {
                     mw[0] = mw[1] = 0xffffffffu;  // membership is applied by the MMA
                     if (p.causal) {
-                        mbar_wait(&bars[C::B_MFULL + s], (uint32_t)((c / S_) & 1));
-                        const uint32_t* meta = sMeta + s * kChunk;
+                        mbar_wait(&bars[C::B_MFULL + (int)(c % VS)], (uint32_t)((c / VS) & 1));
+                        const uint32_t* meta = sMeta + (int)(c % VS) * kChunk;
                         int lo = 0, hi = kChunk;  // keys ascending: visible = prefix with key <= qrow
                         while (lo < hi) {
                             const int mid = (lo + hi) >> 1;
