@@ -363,6 +363,12 @@ cudaError_t run_select(const vecattn_problem_t* p, const vecattn_select_params_t
                 delete ss;
                 // VECATTN_TOPK_FORCE_FALLBACK=1 (tests): no candidate room -> every row takes the
                 // radix fallback, which must give the same selection
+                // candidate counts of every (row, segment, warp set) slice: causal units above
+                // the diagonal never run, so their slices must read as empty
+#ifndef VA_TEST_NO_NCAND_CLEAR  // (build knob used once to check that tests/test_gpu_stale_ws.py catches the stale read)
+                if (e == cudaSuccess)
+                    e = cudaMemsetAsync(w.tk_ncand, 0, (size_t)R * 4 * 2 * (size_t)((p->N + kTkCandSeg - 1) / kTkCandSeg), cs);
+#endif
                 const int64_t cap_keep = sp.cand_cap;
                 if (getenv("VECATTN_TOPK_FORCE_FALLBACK")) sp.cand_cap = 0;
                 if (e == cudaSuccess) e = run(va::EPI_TK_CAND, 0);
