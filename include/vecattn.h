@@ -46,7 +46,7 @@ typedef struct CUstream_st* vecattn_stream_t; /* ABI-identical to cudaStream_t; 
 typedef enum {
     VECATTN_OK = 0,
     VECATTN_ERR_INVALID_ARGUMENT = 1, /* NULL pointer, pq not in {64,128}, alpha < 0 or NaN, bk not in
-                                         {16,32,64}, gk < 1, TOPK with neither topk > 0 nor
+                                         {8,...,256} (powers of 2), gk < 1, TOPK with neither topk > 0 nor
                                          keep_frac in (0,1], Hq % Hkv != 0, scale < 0 or NaN          */
     VECATTN_ERR_SHAPE = 2,            /* B, N < 1; D not in {64,128}; N >= 2^28; Hq > 1024; pointer not
                                          16-byte aligned; B*Hkv*N >= 2^31                              */
@@ -72,7 +72,7 @@ typedef enum {
 typedef struct {
     int32_t mode;                /* vecattn_sel_mode_t                                              */
     int32_t pq;                  /* vector size P_q = query-block size, 64 or 128   */
-    int32_t bk;                  /* Alg. 1 K-tile size B_K: 16, 32 or 64 (paper default 16)         */
+    int32_t bk;                  /* Alg. 1 K-tile size B_K: 8, 16, 32, 64, 128 or 256 (paper: 16)    */
     int32_t gk;                  /* Alg. 1 K-tiles per group G_K >= 1 (16 VLM, 8192 DiT)     */
     float alpha;                 /* minS filtering ratio (Eq. 3), >= 0, in scaled-logit units (R4)  */
     const float* alpha_per_head; /* HOST pointer [Hq] or NULL; overrides alpha per query head (Eq. 4) */

@@ -89,7 +89,8 @@ vecattn_status_t check_select(const vecattn_problem_t* p, const vecattn_select_p
     if (!s) return VECATTN_ERR_INVALID_ARGUMENT;
     if (s->pq != 64 && s->pq != 128) return VECATTN_ERR_INVALID_ARGUMENT;
     if (s->mode < 0 || s->mode > 2) return VECATTN_ERR_INVALID_ARGUMENT;
-    if (s->mode == VECATTN_SEL_MINS_ALG1 && s->bk != 16 && s->bk != 32 && s->bk != 64)
+    if (s->mode == VECATTN_SEL_MINS_ALG1 && s->bk != 8 && s->bk != 16 && s->bk != 32 &&
+        s->bk != 64 && s->bk != 128 && s->bk != 256)
         return VECATTN_ERR_INVALID_ARGUMENT;
     if (s->mode == VECATTN_SEL_MINS_ALG1 && s->gk < 1) return VECATTN_ERR_INVALID_ARGUMENT;
     if (s->mode != VECATTN_SEL_TOPK) {
@@ -124,7 +125,8 @@ struct SelectWs {
 
 constexpr int kTkStride = 8;         // windowed TOPK: 1 of every 8 keys in the sampled passes
 constexpr int64_t kTkCandSeg = 16384;  // candidate pass key segment
-int64_t tk_cand_cap(const vecattn_problem_t* p) { return std::min<int64_t>(p->N, 16384); }
+// a multiple of 128: the per-(segment, warp set) slices start 16-B aligned (vector candidate stores)
+int64_t tk_cand_cap(const vecattn_problem_t* p) { return (std::min<int64_t>(p->N, 16384) + 127) / 128 * 128; }
 
 SelectWs carve_select(const vecattn_problem_t* p, int32_t pq, void* base, bool topk = false) {
     const int64_t BH = p->B * p->Hq, Np = n_pooled(p, pq), R = BH * Np;
@@ -273,6 +275,8 @@ vecattn_status_t fill_select_params(const vecattn_problem_t* p, const vecattn_se
     sp.tk_ncand = w.tk_ncand;
     sp.tk_fail = w.tk_fail;
     sp.tk_nfail = w.tk_nfail;
+    sp.tk_sigma = 4.5f;
+    if (const char* ev = getenv("VECATTN_TOPK_SIGMA")) sp.tk_sigma = (float)atof(ev);  // experiments (scripts)
     sp.topk = s ? s->topk : 0;
     sp.keep_frac = s ? s->keep_frac : 0.f;
     const float scale = eff_scale(p);
@@ -397,8 +401,16 @@ cudaError_t run_select(const vecattn_problem_t* p, const vecattn_select_params_t
                         mx = std::max(mx, nc[r]);
                         over += nc[r] > (uint32_t)w.cand_cap;
                     }
-                    fprintf(stderr, "[topk window] rows %lld failed %d overflow %u mean cand %.0f max %u\n", (long long)R, nf,
-                            over, sn / R, mx);
+                    uint64_t hsh = 1469598103934665603ull;  // FNV-1a of the window bounds' bits
+                    for (int64_t r = 0; r < R; ++r) {
+                        uint32_t b2[2];
+                        memcpy(&b2[0], &lo[r], 4);
+                        memcpy(&b2[1], &hi[r], 4);
+                        hsh = (hsh ^ b2[0]) * 1099511628211ull;
+                        hsh = (hsh ^ b2[1]) * 1099511628211ull;
+                    }
+                    fprintf(stderr, "[topk window] rows %lld failed %d overflow %u mean cand %.0f max %u window hash %016llx\n",
+                            (long long)R, nf, over, sn / R, mx, (unsigned long long)hsh);
                     std::vector<uint32_t> smx(4), smn(4), h(512);
                     std::vector<float> tp(4), iw(4);
                     cudaMemcpy(smx.data(), w.tk_smax, 16, cudaMemcpyDeviceToHost);

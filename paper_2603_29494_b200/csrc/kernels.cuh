@@ -69,6 +69,7 @@ struct SelectParams {
     uint32_t* tk_ncand;            // [R] visible scores in [lo, hi]
     uint32_t* tk_fail;             // [R] 1: the window missed the k-th largest (fallback radix)
     int* tk_nfail;                 // rows with tk_fail
+    float tk_sigma;                // window half-width in binomial sigmas of the sample rank (+8 ranks)
     float alpha_raw[1024];         // per q head: alpha / scale (raw-accumulator units)
 };
 

@@ -28,6 +28,7 @@
 #include "kernels.cuh"
 
 #include <math.h>
+#include <stdlib.h>
 
 namespace va {
 
@@ -186,6 +187,7 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
         const int64_t G = (int64_t)p.bk * (int64_t)p.gk;
         int64_t next_reset = k_begin;              // Alg. 1 group boundaries (multiples of G)
         float m_run = -INFINITY;                   // ALG1 running max / EPI_MAX row max
+        float span_mx = -INFINITY;                 // ALG1, B_K > 64: rowmax of the current sub-tile
         if (EPI == EPI_ALG1 && p.split && row_ok) {
             // K-split of a single-group row (G >= N): this segment continues the group that
             // started at key 0, so the running max starts at the max of the earlier segments
@@ -198,6 +200,9 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
         float mn_run = INFINITY;                   // EPI_TK_MINMAX row min
         float tk_a = 0.f, tk_b = 0.f;              // SHIST: top*invw, invw; CAND: lo, hi
         uint32_t above = 0, ncand = 0;             // CAND counters
+        float cb_v[4] = {0.f, 0.f, 0.f, 0.f};      // CAND: buffered candidates (scores, indices)
+        int32_t cb_i[4] = {0, 0, 0, 0};
+        uint32_t nb = 0;
         if constexpr (EPI == EPI_TK_SHIST) {
             if (row_ok) {
                 tk_b = p.tk_invw[grow];
@@ -219,6 +224,8 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
         const int64_t slice = 2 * seg + eset;
         float* cand_row = (EPI == EPI_TK_CAND) ? p.tk_cand + grow * p.cand_cap + slice * subcap : nullptr;
         int32_t* cidx_row = (EPI == EPI_TK_CAND) ? p.tk_cidx + grow * p.cand_cap + slice * subcap : nullptr;
+        const bool vec_ok = (EPI == EPI_TK_CAND) && (subcap & 3) == 0 && ((uintptr_t)cand_row & 15u) == 0 &&
+                            ((uintptr_t)cidx_row & 15u) == 0;
         uint32_t tk_prefix = 0, tk_krem = 0, tk_taken = 0;
         unsigned long long cnt = 0;
         uint32_t* hist = reinterpret_cast<uint32_t*>(smem + C::kOffHist);
@@ -296,17 +303,47 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
                             if (j >= nvis) v[j] = -INFINITY;
                     }
                     // rowmax of every B_K sub-tile first (independent chains), then Alg. 1's
-                    // sequential running max and threshold per sub-tile
-                    float gmx[64 / BK];
+                    // sequential running max and threshold per sub-tile.  B_K > 64: the sub-tile
+                    // spans BK / 64 chunks of this TMEM tile (BK divides BN), so its rowmax is
+                    // taken once, at its first chunk, by reading the later chunks ahead.
+                    constexpr int kSub = BK < 64 ? BK : 64;
+                    float gmx[64 / kSub];
+                    if constexpr (BK > 64) {
+                        if ((c * 64) % BK == 0) {
+                            float a = -INFINITY, b = -INFINITY;
 #pragma unroll
-                    for (int g = 0; g < 64 / BK; ++g) {
-                        float a = -INFINITY, b = -INFINITY;
+                            for (int j = 0; j < 64; j += 4) {
+                                a = fmax3(a, v[j], v[j + 1]);
+                                b = fmax3(b, v[j + 2], v[j + 3]);
+                            }
+#pragma unroll 1
+                            for (int c2 = 1; c2 < BK / 64; ++c2) {
+                                uint32_t ua[32], ub[32];
+                                tmem_ld32(taddr + c2 * 64, ua);
+                                tmem_ld32(taddr + c2 * 64 + 32, ub);
+                                tmem_ld_wait();
+                                const int64_t nv2 = vis_end - (kc + c2 * 64);
+                                const int n2 = row_ok ? (int)max((int64_t)0, min((int64_t)64, nv2)) : 0;
 #pragma unroll
-                        for (int j = 0; j < BK; j += 4) {
-                            a = fmax3(a, v[g * BK + j], v[g * BK + j + 1]);
-                            b = fmax3(b, v[g * BK + j + 2], v[g * BK + j + 3]);
+                                for (int j = 0; j < 32; ++j) {
+                                    if (j < n2) a = fmaxf(a, __uint_as_float(ua[j]));
+                                    if (32 + j < n2) b = fmaxf(b, __uint_as_float(ub[j]));
+                                }
+                            }
+                            span_mx = fmaxf(a, b);
                         }
-                        gmx[g] = fmaxf(a, b);
+                        gmx[0] = span_mx;
+                    } else {
+#pragma unroll
+                        for (int g = 0; g < 64 / BK; ++g) {
+                            float a = -INFINITY, b = -INFINITY;
+#pragma unroll
+                            for (int j = 0; j < BK; j += 4) {
+                                a = fmax3(a, v[g * BK + j], v[g * BK + j + 1]);
+                                b = fmax3(b, v[g * BK + j + 2], v[g * BK + j + 3]);
+                            }
+                            gmx[g] = fmaxf(a, b);
+                        }
                     }
                     // keep = s >= m_S - alpha (R1) <=> the sign bit of s - thr is clear:
                     // for finite thr the IEEE difference is negative exactly when s < thr (no
@@ -314,15 +351,15 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
                     // bits are shifted in (funnel shift) and inverted/bit-reversed per word.
                     uint32_t sg0 = 0u, sg1 = 0u;
 #pragma unroll
-                    for (int sub = 0; sub < 64; sub += BK) {
+                    for (int sub = 0; sub < 64; sub += kSub) {
                         if (kc + sub == next_reset) {  // new group of G_K tiles: m_S <- -inf
                             m_run = -INFINITY;
                             next_reset += G;
                         }
-                        m_run = fmaxf(m_run, gmx[sub / BK]);      // m_S <- max(m_S, rowmax(S_tile))
+                        m_run = fmaxf(m_run, gmx[sub / kSub]);    // m_S <- max(m_S, rowmax(S_tile))
                         const float nthr = alpha_raw - m_run;     // -(m_S - alpha)
 #pragma unroll
-                        for (int j = sub; j < sub + BK; j += 2) {
+                        for (int j = sub; j < sub + kSub; j += 2) {
                             const float2 d = fadd2(make_float2(v[j], v[j + 1]), make_float2(nthr, nthr));
                             if (j < 32) {
                                 sg0 = __funnelshift_l(__float_as_uint(d.x), sg0, 1);
@@ -434,29 +471,52 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
                     // lanes are consecutive rows), then each thread walks its set bits (~4% of
                     // scores) reading the stage with a dynamic index
                     float* stg = reinterpret_cast<float*>(hist) + eset * 64 * 128 + r;
+#ifdef VA_TK_CAND_NOSTORE
+                    ncand += __popc(in0) + __popc(in1);
+                    if (false) {
+#else
                     if ((in0 | in1) != 0u) {
+#endif
 #pragma unroll
                         for (int j = 0; j < 64; ++j) stg[j * 128] = v[j];
+                        // candidates go through a 4-entry register buffer and leave as one 16-B
+                        // store of scores + one of indices (a quarter of the scattered store
+                        // transactions of per-candidate 4-B stores; each lane is its own row)
                         const uint32_t cap = (uint32_t)subcap;
-                        uint32_t m = in0;
-                        while (m) {
-                            const int j = __ffs(m) - 1;
-                            m &= m - 1u;
-                            if (ncand < cap) {
-                                cand_row[ncand] = stg[j * 128];
-                                cidx_row[ncand] = (int32_t)(kc + j);
+#pragma unroll
+                        for (int half = 0; half < 2; ++half) {
+                            uint32_t m = half ? in1 : in0;
+                            while (m) {
+                                const int j = 32 * half + __ffs(m) - 1;
+                                m &= m - 1u;
+                                if (ncand < cap) {
+                                    const float sv = stg[j * 128];
+                                    const int32_t si = (int32_t)(kc + j);
+                                    cb_v[0] = nb == 0 ? sv : cb_v[0];
+                                    cb_v[1] = nb == 1 ? sv : cb_v[1];
+                                    cb_v[2] = nb == 2 ? sv : cb_v[2];
+                                    cb_v[3] = nb == 3 ? sv : cb_v[3];
+                                    cb_i[0] = nb == 0 ? si : cb_i[0];
+                                    cb_i[1] = nb == 1 ? si : cb_i[1];
+                                    cb_i[2] = nb == 2 ? si : cb_i[2];
+                                    cb_i[3] = nb == 3 ? si : cb_i[3];
+                                    if (++nb == 4) {
+                                        const uint32_t at = ncand - 3u;  // a multiple of 4
+                                        if (vec_ok) {
+                                            *reinterpret_cast<float4*>(cand_row + at) = make_float4(cb_v[0], cb_v[1], cb_v[2], cb_v[3]);
+                                            *reinterpret_cast<int4*>(cidx_row + at) = make_int4(cb_i[0], cb_i[1], cb_i[2], cb_i[3]);
+                                        } else {
+#pragma unroll
+                                            for (int e = 0; e < 4; ++e) {
+                                                cand_row[at + e] = cb_v[e];
+                                                cidx_row[at + e] = cb_i[e];
+                                            }
+                                        }
+                                        nb = 0;
+                                    }
+                                }
+                                ++ncand;
                             }
-                            ++ncand;
-                        }
-                        m = in1;
-                        while (m) {
-                            const int j = 32 + __ffs(m) - 1;
-                            m &= m - 1u;
-                            if (ncand < cap) {
-                                cand_row[ncand] = stg[j * 128];
-                                cidx_row[ncand] = (int32_t)(kc + j);
-                            }
-                            ++ncand;
                         }
                     }
                     w0 = ab0;  // keys above the window are kept whatever the k-th largest is
@@ -541,6 +601,13 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
                     atomicMin(&p.tk_smin[grow], f32_order_key(mn_run));
                 }
             } else if constexpr (EPI == EPI_TK_CAND) {
+                const uint32_t at = min(ncand, (uint32_t)subcap) - nb;  // the buffered tail
+#pragma unroll
+                for (int e = 0; e < 3; ++e)
+                    if ((uint32_t)e < nb) {
+                        cand_row[at + e] = cb_v[e];
+                        cidx_row[at + e] = cb_i[e];
+                    }
                 if (above) atomicAdd(&p.tk_cabove[grow], above);
                 p.tk_ncand[grow * 2 * p.n_seg + slice] = ncand;
             } else if constexpr (EPI == EPI_TK_SHIST) {
@@ -625,9 +692,12 @@ template <int D>
 static cudaError_t launch_sel_d(const SelectParams& p, int epi, cudaStream_t st) {
     switch (epi) {
         case EPI_ALG1:
+            if (p.bk == 8) return launch_sel_t<D, 256, 3, EPI_ALG1, 8>(p, st);
             if (p.bk == 16) return launch_sel_t<D, 256, 3, EPI_ALG1, 16>(p, st);
             if (p.bk == 32) return launch_sel_t<D, 256, 3, EPI_ALG1, 32>(p, st);
             if (p.bk == 64) return launch_sel_t<D, 256, 3, EPI_ALG1, 64>(p, st);
+            if (p.bk == 128) return launch_sel_t<D, 256, 3, EPI_ALG1, 128>(p, st);
+            if (p.bk == 256) return launch_sel_t<D, 256, 3, EPI_ALG1, 256>(p, st);
             return cudaErrorInvalidValue;
         case EPI_MAX: return launch_sel_t<D, 256, 3, EPI_MAX>(p, st);
         case EPI_THRESH: return launch_sel_t<D, 256, 3, EPI_THRESH>(p, st);
@@ -725,9 +795,11 @@ __global__ void __launch_bounds__(256) tk_rows_kernel(const __grid_constant__ Se
     const uint32_t* h1 = p.tk_hist + row * 256;
     // level-1 binning (stage 1's, recomputed: tk_top / tk_invw hold level 2 after stage 2)
     const float top1 = smax, invw1 = (smax - smin) > 0.f ? 255.f / (smax - smin) : 0.f;
-    // window ranks [ks - d, ks + d] in the sample, d = 6 sigma + 4 (binomial rank of a sample quantile)
+    // window ranks [ks - d, ks + d] in the sample, d = c sigma + 8 (binomial rank spread of a
+    // sample quantile; c = tk_sigma, 4.5 by default: measured |z| <= 3.5 over 48K rows,
+    // profiles/topk_window_r02.md; a missed row takes the exact radix fallback)
     const double pr = min(1.0, ki / (double)vis_real);
-    const double d = 6.0 * sqrt((double)ns * pr * (1.0 - pr)) + 8.0;
+    const double d = (double)p.tk_sigma * sqrt((double)ns * pr * (1.0 - pr)) + 8.0;
     const double r_lo = ks - d, r_hi = ks + d;
     if (stage == 2) {
         // level-1 bins ba..bb hold sample ranks r_lo..r_hi (counted from the top: bin 0 = the
@@ -798,11 +870,190 @@ __global__ void __launch_bounds__(256) tk_rows_kernel(const __grid_constant__ Se
     p.tk_lo[row] = lo == -INFINITY ? -INFINITY : lo - fabsf(lo) * e - 1e-30f;
 }
 
-// One warp per row: exact k'-th largest (k' = k - #above) among the window candidates, radix
-// select on order keys (4 x 8-bit digits, warp-private shared histogram), then the kept
-// candidates' bits: key > theta, and the k_rem lowest-index keys == theta (R12).  Candidates
-// are in slices (candidate-pass segment x warp set), so ties are ranked by index explicitly.
+// Stages 2 and 3 of tk_rows_kernel with one warp per row: the histogram walks become warp
+// scans (lane l owns 8 consecutive bins; coalesced reads), same arithmetic and the same window.
+// Counts are doubled so that the half pieces of stage 3 stay integers.
+struct TkScan {
+    int hit_lo, hit_hi;  // first index whose running count reaches T_lo / T_hi in this segment, or -1
+    uint32_t total;      // doubled counts of the segment
+};
+// segment a[s0 .. s0 + n) (n <= 256) with doubled counts, running doubled count cum2 before it
+VA_DEV TkScan tk_warp_scan(const uint32_t* a, int s0, int n, uint32_t cum2, double t_lo, double t_hi, int lane) {
+    uint32_t vv[8];
+    uint32_t own = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const int x = 8 * lane + t;
+        vv[t] = x < n ? 2u * a[s0 + x] : 0u;
+        own += vv[t];
+    }
+    uint32_t incl = own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    TkScan r;
+    r.total = __shfl_sync(0xffffffffu, incl, 31);
+    const double base = (double)cum2;
+    const uint32_t excl = incl - own;
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+        const double T = which ? t_hi : t_lo;
+        const unsigned ball = __ballot_sync(0xffffffffu, base + (double)incl >= T);
+        int hit = -1;
+        if (ball) {
+            const int L = __ffs(ball) - 1;
+            int loc = 7;
+            double c = base + (double)excl;
+            for (int t = 0; t < 8; ++t) {
+                c += (double)vv[t];
+                if (c >= T) {
+                    loc = t;
+                    break;
+                }
+            }
+            hit = 8 * L + __shfl_sync(0xffffffffu, loc, L);
+        }
+        if (which) r.hit_hi = hit;
+        else r.hit_lo = hit;
+    }
+    return r;
+}
+
+__global__ void __launch_bounds__(256) tk_rows_warp_kernel(const __grid_constant__ SelectParams p, int stage, int stride) {
+    const int64_t R = p.BH * p.Np;
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (row >= R) return;
+    const int64_t i = row % p.Np;
+    const int64_t vis_real = p.causal ? min(p.N_real, (i + 1) * (int64_t)p.pq) : p.N_real;
+    const int64_t ns = (vis_real + stride - 1) / stride;
+    const float smax = f32_from_order_key(p.tk_smax[row]), smin = f32_from_order_key(p.tk_smin[row]);
+    const double ki = (double)tk_budget(p, vis_real);
+    const double ks = ki * (double)ns / (double)vis_real;
+    const uint32_t* h1 = p.tk_hist + row * 256;
+    const float top1 = smax, invw1 = (smax - smin) > 0.f ? 255.f / (smax - smin) : 0.f;
+    const double pr = min(1.0, ki / (double)vis_real);
+    const double d = (double)p.tk_sigma * sqrt((double)ns * pr * (1.0 - pr)) + 8.0;
+    const double r_lo = ks - d, r_hi = ks + d;
+    if (stage == 2) {
+        // doubled counts against doubled thresholds: the same first crossings as the thread walk
+        const TkScan sc = tk_warp_scan(h1, 0, 256, 0u, 2.0 * r_lo, 2.0 * r_hi, lane);
+        const int ba = sc.hit_lo < 0 ? 255 : sc.hit_lo;
+        const int bb = sc.hit_hi < 0 ? 255 : sc.hit_hi;
+        if (lane == 0) {
+            const float top2 = invw1 > 0.f ? top1 - ((float)ba - 0.5f) / invw1 : top1;
+            const float invw2 = invw1 > 0.f ? invw1 * 256.f / (float)(bb - ba + 1) : 0.f;
+            p.tk_lo[row] = (float)ba;
+            p.tk_hi[row] = (float)bb;
+            p.tk_top[row] = top2;
+            p.tk_invw[row] = invw2;
+        }
+        return;
+    }
+    const int ba = (int)p.tk_lo[row], bb = (int)p.tk_hi[row];
+    const uint32_t* h2 = p.tk_hist + (R + row) * 256;
+    const float top2 = p.tk_top[row], invw2 = p.tk_invw[row];
+    const double T_hi = 2.0 * r_lo, T_lo = 2.0 * r_hi;  // hi: where rank r_lo is reached; lo: r_hi
+    float hi = INFINITY, lo = -INFINITY;
+    bool have_hi = r_lo < 1.0, have_lo = false;
+    uint32_t cum2 = 0;
+    // one segment of pieces: the first crossings give the edges (edge(x, upper?) of piece x)
+    auto seg = [&](const uint32_t* a, int s0, int n, auto up, auto dn) {
+        if (n <= 0 || have_lo) return;
+        const TkScan sc = tk_warp_scan(a, s0, n, cum2, T_hi, T_lo, lane);
+        if (!have_hi && sc.hit_lo >= 0) {
+            hi = up(sc.hit_lo);
+            have_hi = true;
+        }
+        if (!have_lo && sc.hit_hi >= 0) {
+            lo = dn(sc.hit_hi);
+            have_lo = true;
+        }
+        cum2 += sc.total;
+    };
+    auto piece = [&](uint32_t cnt2, float edge) {  // one piece of doubled count cnt2
+        if (have_lo) return;
+        if (!have_hi && (double)(cum2 + cnt2) >= T_hi) {
+            hi = edge;
+            have_hi = true;
+        }
+        if ((double)(cum2 + cnt2) >= T_lo) {
+            lo = edge;
+            have_lo = true;
+        }
+        cum2 += cnt2;
+    };
+    if (invw1 <= 0.f) {  // all sampled scores equal: one bin
+        seg(h1, 0, 256, [&](int) { return top1; }, [&](int) { return top1; });
+    } else {
+        auto up1 = [&](int x) { return top1 - ((float)x - 0.5f) / invw1; };
+        auto dn1 = [&](int x) { return top1 - ((float)x + 0.5f) / invw1; };
+        seg(h1, 0, ba, up1, dn1);
+        // level-1 bins ba..bb as the 256 level-2 sub-bins; level-1 scores of the range that
+        // level 2 rounded out go half to each edge
+        uint32_t in1 = 0, in2 = 0;
+        for (int x = lane; x < 256; x += 32) {
+            in1 += (x >= ba && x <= bb) ? h1[x] : 0u;
+            in2 += h2[x];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            in1 += __shfl_xor_sync(0xffffffffu, in1, o);
+            in2 += __shfl_xor_sync(0xffffffffu, in2, o);
+        }
+        const uint32_t rest = in1 > in2 ? in1 - in2 : 0u;  // doubled half = rest
+        const float dnb = top1 - ((float)bb + 0.5f) / invw1;
+        piece(rest, up1(ba));
+        seg(h2, 0, 256, [&](int y) { return top2 - ((float)y - 0.5f) / invw2; },
+            [&](int y) { return top2 - ((float)y + 0.5f) / invw2; });
+        piece(rest, dnb);
+        seg(h1, bb + 1, 255 - bb, [&](int x) { return up1(bb + 1 + x); }, [&](int x) { return dn1(bb + 1 + x); });
+    }
+    if (lane == 0) {
+        const float e = 1.0f / 65536.0f;
+        p.tk_hi[row] = hi == INFINITY ? INFINITY : hi + fabsf(hi) * e + 1e-30f;
+        p.tk_lo[row] = lo == -INFINITY ? -INFINITY : lo - fabsf(lo) * e - 1e-30f;
+    }
+}
+
+// One warp per row: exact k'-th largest (k' = k - #above) among the window candidates, then
+// the kept candidates' bits: key > theta, and the k_rem lowest-index keys == theta (R12).
+// Candidates are in slices (candidate-pass segment x warp set), so ties are ranked by index
+// explicitly.
+//   fast path: every candidate's order key lies in [klo, khi], where the window is locally
+//     ~uniform, so ONE histogram pass with linear bins over that range (the top 8 significant
+//     bits of key - klo) leaves ~n/200 candidates in the bin holding the k'-th largest; those
+//     are ranked exactly by (key desc, index asc) in shared memory (R12's order).
+//   radix path (the bin holds > kTkBinCap candidates, e.g. mass ties): radix select on order
+//     keys (8-bit digits, warp-private shared histogram) from the first digit where klo and
+//     khi differ.
 constexpr int kTkMaxTies = 1024;
+constexpr uint32_t kTkBinCap = 512;  // fast path: candidates of the k'-th largest's bin
+__device__ __forceinline__ int tk_pick_bin(const uint32_t* h, uint32_t krem, int lane, uint32_t& cum) {
+    // from the top: lane l owns bins [255 - 8l - 7, 255 - 8l]; returns the bin where the
+    // running count from the top reaches krem, cum = count strictly above it
+    uint32_t own = 0;
+    for (int t = 0; t < 8; ++t) own += h[255 - 8 * lane - t];
+    uint32_t incl = own;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t excl = incl - own;
+    const unsigned ball = __ballot_sync(0xffffffffu, incl >= krem);
+    const int L = __ffs(ball) - 1;
+    cum = __shfl_sync(0xffffffffu, excl, L);
+    int bin = 255 - 8 * L;
+    for (int t = 0; t < 8; ++t, --bin) {
+        const uint32_t hc = h[bin];
+        if (cum + hc >= krem) break;
+        cum += hc;
+    }
+    return bin;
+}
+
 __global__ void __launch_bounds__(256) tk_exact_kernel(const __grid_constant__ SelectParams p) {
     __shared__ uint32_t hist[8][256];
     __shared__ int32_t tie_idx[8][kTkMaxTies];
@@ -833,9 +1084,77 @@ __global__ void __launch_bounds__(256) tk_exact_kernel(const __grid_constant__ S
     const int32_t* cidx = p.tk_cidx + row * p.cand_cap;
     uint32_t krem = (uint32_t)(ki - above);
     uint32_t* h = hist[wid];
+    uint32_t* bm = p.bitmask + row * p.words_per_row;
+    int32_t* tl = tie_idx[wid];
+    const uint32_t klo = f32_order_key(p.tk_lo[row]), khi = f32_order_key(p.tk_hi[row]);
+
+    // ---------------------------------------------------------------- fast path
+    const uint32_t W = khi - klo;
+    const int shb = max(0, (32 - __clz((int)W)) - 8);  // (key - klo) >> shb < 256
+    for (int bin = lane; bin < 256; bin += 32) h[bin] = 0u;
+    __syncwarp();
+    for (int64_t sg = 0; sg < nsl; ++sg) {
+        const int64_t c = p.tk_ncand[row * nsl + sg];
+        const float* cs = cand + sg * subcap;
+        for (int64_t x = lane; x < c; x += 32) {
+            const uint32_t d = min(f32_order_key(cs[x]) - klo, W);
+            atomicAdd(&h[d >> shb], 1u);
+        }
+    }
+    __syncwarp();
+    uint32_t cum;
+    const int bb = tk_pick_bin(h, krem, lane, cum);
+    const uint32_t m = h[bb];
+    __syncwarp();
+    if (m <= kTkBinCap) {
+        const uint32_t kb = krem - cum;  // to take from bin bb (1 <= kb <= m)
+        uint32_t* tu = reinterpret_cast<uint32_t*>(tl + kTkBinCap);
+        uint32_t nm = 0;
+        for (int64_t sg = 0; sg < nsl; ++sg) {
+            const int64_t c = p.tk_ncand[row * nsl + sg];
+            const float* cs = cand + sg * subcap;
+            const int32_t* is = cidx + sg * subcap;
+            for (int64_t x0 = 0; x0 < c; x0 += 32) {
+                const int64_t x = x0 + lane;
+                const uint32_t u = x < c ? f32_order_key(cs[x]) : 0u;
+                const int bin = x < c ? (int)(min(u - klo, W) >> shb) : -1;
+                if (bin > bb) {
+                    const int32_t key = is[x];
+                    atomicOr(&bm[key >> 5], 1u << (key & 31));
+                }
+                const bool inb = bin == bb;
+                const unsigned tb = __ballot_sync(0xffffffffu, inb);
+                if (inb) {
+                    const uint32_t slot = nm + __popc(tb & ((1u << lane) - 1u));
+                    tl[slot] = is[x];
+                    tu[slot] = u;
+                }
+                nm += __popc(tb);
+            }
+        }
+        __syncwarp();
+        // rank in (key desc, index asc); the kb first are kept.  theta = key of rank kb - 1.
+        for (uint32_t t = lane; t < nm; t += 32) {
+            const uint32_t ut = tu[t];
+            const int32_t it = tl[t];
+            uint32_t rank = 0;
+            for (uint32_t o = 0; o < nm; ++o) {
+                const uint32_t uo = tu[o];
+                rank += (uo > ut || (uo == ut && tl[o] < it)) ? 1u : 0u;
+            }
+            if (rank < kb) atomicOr(&bm[it >> 5], 1u << (it & 31));
+            if (rank == kb - 1) p.tk_prefix[row] = ut;
+        }
+        if (lane == 0) {
+            p.tk_krem[row] = 0u;  // unused downstream on this path
+            p.counts[row] = (unsigned long long)ki;  // top-k keeps exactly k_i keys
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------- radix path
     // every candidate lies in [lo, hi]: the leading bytes their order keys share with both
     // bounds are known, so the radix starts at the first byte where the bounds differ
-    const uint32_t klo = f32_order_key(p.tk_lo[row]), khi = f32_order_key(p.tk_hi[row]);
     int first = 0;
     while (first < 3 && (klo >> (24 - 8 * first)) == (khi >> (24 - 8 * first))) ++first;
     uint32_t prefix = first > 0 ? (klo >> (32 - 8 * first)) : 0u;
@@ -852,32 +1171,13 @@ __global__ void __launch_bounds__(256) tk_exact_kernel(const __grid_constant__ S
             }
         }
         __syncwarp();
-        // from the top: lane l owns bins [255 - 8l - 7, 255 - 8l]
-        uint32_t own = 0;
-        for (int t = 0; t < 8; ++t) own += h[255 - 8 * lane - t];
-        uint32_t incl = own;  // inclusive prefix over lanes (bins from the top)
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const uint32_t excl = incl - own;
-        const unsigned ball = __ballot_sync(0xffffffffu, incl >= krem);
-        const int L = __ffs(ball) - 1;  // first lane whose bins reach krem
-        uint32_t cum = __shfl_sync(0xffffffffu, excl, L);
-        int bin = 255 - 8 * L;
-        for (int t = 0; t < 8; ++t, --bin) {
-            const uint32_t hc = h[bin];
-            if (cum + hc >= krem) break;
-            cum += hc;
-        }
+        const int bin = tk_pick_bin(h, krem, lane, cum);
         prefix = (prefix << 8) | (uint32_t)bin;
         krem -= cum;
         __syncwarp();
     }
     // kept candidates -> bitmask (the keys above the window were set by the candidate pass);
     // ties (key == theta) are gathered and the krem lowest indices kept
-    uint32_t* bm = p.bitmask + row * p.words_per_row;
-    int32_t* tl = tie_idx[wid];
     uint32_t nt = 0;
     for (int64_t sg = 0; sg < nsl; ++sg) {
         const int64_t c = p.tk_ncand[row * nsl + sg];
@@ -939,7 +1239,10 @@ cudaError_t launch_tk_sample_k(const void* k, void* ks, int64_t BHkv, int64_t N,
 cudaError_t launch_tk_rows(const SelectParams& p, int stage, int stride, cudaStream_t st) {
     const int64_t R = p.BH * p.Np;
     if (R <= 0) return cudaSuccess;
-    tk_rows_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(p, stage, stride);
+    if (stage >= 2 && !getenv("VECATTN_TK_ROWS_THREAD"))  // (env: the thread-per-row walk, A/B only)
+        tk_rows_warp_kernel<<<(unsigned)((R + 7) / 8), 256, 0, st>>>(p, stage, stride);
+    else
+        tk_rows_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(p, stage, stride);
     return cudaGetLastError();
 }
 

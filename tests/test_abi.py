@@ -90,7 +90,8 @@ def test_argument_errors_are_synchronous(lib):
         assert lib.vecattn_select(ctypes.byref(p2), ctypes.byref(sp), fake, fake, fake, None, 0, fake, fake,
                                   ws_bytes, st) == code
     for cfg, code in [(va.SelectConfig(pq=32), 1), (va.SelectConfig(alpha=-1.0), 1),
-                      (va.SelectConfig(bk=8), 1), (va.SelectConfig(gk=0), 1),
+                      (va.SelectConfig(bk=4), 1), (va.SelectConfig(bk=48), 1), (va.SelectConfig(bk=512), 1),
+                      (va.SelectConfig(gk=0), 1),
                       (va.SelectConfig(mode="topk", topk=0, keep_frac=0.0), 1),
                       (va.SelectConfig(alpha=float("nan")), 1)]:
         s2 = cfg.params()

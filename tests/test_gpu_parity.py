@@ -84,6 +84,11 @@ SEL_CASES = [
     ("gauss", 1, 1, 1, 2048, 64, 64, False, "topk", 16, 16, 0.0, 100, 0.0),
     ("video", 1, 2, 1, 4096, 128, 64, False, "alg1", 32, 4, 1.0, 0, 0.0),
     ("video", 1, 2, 1, 4096, 128, 64, True, "alg1", 64, 3, 1.0, 0, 0.0),
+    # B_K below and above one 64-key TMEM chunk (B_K > 64: sub-tile max read ahead across chunks)
+    ("video", 1, 2, 1, 5000 + 33, 128, 64, True, "alg1", 8, 5, 1.0, 0, 0.0),
+    ("video", 1, 2, 2, 5000 + 33, 128, 64, False, "alg1", 128, 3, 1.0, 0, 0.0),
+    ("video", 1, 2, 1, 6000 + 7, 64, 64, True, "alg1", 256, 2, 1.0, 0, 0.0),
+    ("video", 1, 1, 1, 40000 + 37, 128, 64, False, "alg1", 128, 8192, 1.0, 0, 0.0),
     # TOPK rows longer than one 16K-key histogram segment: per-segment histograms are summed
     ("video", 1, 1, 1, 40000 + 37, 128, 64, True, "topk", 16, 16, 0.0, 0, 0.2),
     ("gauss", 1, 1, 1, 33000, 128, 64, False, "topk", 16, 16, 0.0, 500, 0.0),

@@ -18,6 +18,8 @@ CASES = [
     ("gauss", 1, 1, 33000, 128, 64, False, 500, 0.0, 0),
     ("gauss", 2, 1, 5000, 64, 128, True, 0, 0.5, 0),
     ("gauss", 1, 1, 9000, 128, 64, False, 0, 0.25, 37),    # every score repeats: ties at the cut
+    ("gauss", 1, 1, 9000, 128, 64, False, 0, 0.25, 13),    # > 512 in the cut's bin: exact radix path
+    ("gauss", 1, 1, 9000, 128, 64, True, 0, 0.4, 7),       # > 1024 ties: radix fallback rows
     ("gauss", 1, 1, 300, 128, 64, True, 0, 0.9, 0),         # tiny rows, keep ~everything
     ("gauss", 1, 1, 4096, 128, 64, False, 0, 1.0, 0),       # keep all
 ]
