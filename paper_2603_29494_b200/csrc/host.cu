@@ -115,7 +115,8 @@ struct SelectWs {
     uint32_t* tk_hist;
     // windowed TOPK (mode TOPK only)
     void* ks;            // sampled K rows [B*Hkv][Ns][D]
-    uint32_t *tk_smax, *tk_smin, *tk_cabove, *tk_ncand, *tk_fail;
+    void* ks1;           // level-1 sub-sample [B*Hkv][Ns1][D] (1 in kTkStride * kTkSub)
+    uint32_t *tk_smax, *tk_smin, *tk_cabove, *tk_ncand, *tk_fail, *tk_sabove;
     float *tk_top, *tk_invw, *tk_lo, *tk_hi, *tk_cand;
     int32_t* tk_cidx;
     int* tk_nfail;
@@ -124,6 +125,7 @@ struct SelectWs {
 };
 
 constexpr int kTkStride = 8;         // windowed TOPK: 1 of every 8 keys in the sampled passes
+constexpr int kTkSub = 8;            // level 1 (min/max, coarse histogram): every 8th sampled key
 constexpr int64_t kTkCandSeg = 16384;  // candidate pass key segment
 // a multiple of 128: the per-(segment, warp set) slices start 16-B aligned (vector candidate stores)
 int64_t tk_cand_cap(const vecattn_problem_t* p) { return (std::min<int64_t>(p->N, 16384) + 127) / 128 * 128; }
@@ -149,8 +151,8 @@ SelectWs carve_select(const vecattn_problem_t* p, int32_t pq, void* base, bool t
     off += align_up((size_t)R * 4);
     w.tk_hist = reinterpret_cast<uint32_t*>(b + off);
     off += align_up((size_t)R * 256 * 4 * (topk ? 2 : 1));  // windowed TOPK: two histogram levels
-    w.ks = nullptr;
-    w.tk_smax = w.tk_smin = w.tk_cabove = w.tk_ncand = w.tk_fail = nullptr;
+    w.ks = w.ks1 = nullptr;
+    w.tk_smax = w.tk_smin = w.tk_cabove = w.tk_ncand = w.tk_fail = w.tk_sabove = nullptr;
     w.tk_top = w.tk_invw = w.tk_lo = w.tk_hi = w.tk_cand = nullptr;
     w.tk_cidx = nullptr;
     w.tk_nfail = nullptr;
@@ -159,7 +161,10 @@ SelectWs carve_select(const vecattn_problem_t* p, int32_t pq, void* base, bool t
         const int64_t Ns = (p->N + kTkStride - 1) / kTkStride;
         w.ks = b + off;
         off += align_up((size_t)(p->B * p->Hkv * Ns * p->D * 2));
-        uint32_t** u32s[] = {&w.tk_smax, &w.tk_smin, &w.tk_cabove, &w.tk_fail};
+        const int64_t Ns1 = (p->N + kTkStride * kTkSub - 1) / (kTkStride * kTkSub);
+        w.ks1 = b + off;
+        off += align_up((size_t)(p->B * p->Hkv * Ns1 * p->D * 2));
+        uint32_t** u32s[] = {&w.tk_smax, &w.tk_smin, &w.tk_cabove, &w.tk_fail, &w.tk_sabove};
         for (uint32_t** x : u32s) {
             *x = reinterpret_cast<uint32_t*>(b + off);
             off += align_up((size_t)R * 4);
@@ -276,6 +281,8 @@ vecattn_status_t fill_select_params(const vecattn_problem_t* p, const vecattn_se
     sp.tk_fail = w.tk_fail;
     sp.tk_nfail = w.tk_nfail;
     sp.tk_sigma = 4.5f;
+    sp.tk_sigma1 = 8.0f;
+    sp.tk_sabove = w.tk_sabove;
     if (const char* ev = getenv("VECATTN_TOPK_SIGMA")) sp.tk_sigma = (float)atof(ev);  // experiments (scripts)
     sp.topk = s ? s->topk : 0;
     sp.keep_frac = s ? s->keep_frac : 0.f;
@@ -338,31 +345,39 @@ cudaError_t run_select(const vecattn_problem_t* p, const vecattn_select_params_t
             const bool windowed = w.tk_cand != nullptr && !getenv("VECATTN_TOPK_RADIX");
             if (windowed) {
                 const int64_t Ns = (p->N + kTkStride - 1) / kTkStride;
+                // level 1 gets its own hashed-offset sample (every 8th row of the 1-in-8 sample
+                // would sit at a fixed phase of period-64 structure, e.g. 64-wide video frames)
+                const int64_t Ns1 = (p->N + kTkStride * kTkSub - 1) / (kTkStride * kTkSub);
                 e = va::launch_tk_sample_k(k, w.ks, p->B * p->Hkv, p->N, Ns, p->D, kTkStride, cs);
+                if (e == cudaSuccess)
+                    e = va::launch_tk_sample_k(k, w.ks1, p->B * p->Hkv, p->N, Ns1, p->D, kTkStride * kTkSub, cs);
                 if (e == cudaSuccess) e = va::launch_tk_rows(sp, 0, kTkStride, cs);
                 if (e == cudaSuccess) e = cudaMemsetAsync(w.tk_nfail, 0, sizeof(int), cs);
-                SelectParams* ss = new SelectParams(sp);  // sampled passes: K = every kTkStride-th row
-                ss->N = Ns;
-                ss->key_stride = kTkStride;
-                auto run_sampled = [&](int epi, int pass) -> cudaError_t {
+                // sampled passes: K = one row per kTkStride (hashed offsets); level 1 (min/max and
+                // the coarse histogram that places level 2): one per kTkStride * kTkSub
+                SelectParams* ss = new SelectParams(sp);
+                auto run_sampled = [&](int epi, int pass, bool level1) -> cudaError_t {
+                    const int64_t n = level1 ? Ns1 : Ns;
+                    ss->N = n;
+                    ss->key_stride = level1 ? kTkStride * kTkSub : kTkStride;
                     plan_segments(p, s, epi, *ss);
                     // min/max: 4096-key units (atomics merge them); histograms: whole sampled rows
-                    ss->seg_len = epi == va::EPI_TK_SHIST ? (Ns + 255) / 256 * 256
-                                                          : std::min<int64_t>(4096, (Ns + 255) / 256 * 256);
-                    ss->n_seg = (Ns + ss->seg_len - 1) / ss->seg_len;
+                    ss->seg_len = epi == va::EPI_TK_SHIST ? (n + 255) / 256 * 256
+                                                          : std::min<int64_t>(4096, (n + 255) / 256 * 256);
+                    ss->n_seg = (n + ss->seg_len - 1) / ss->seg_len;
                     ss->split = 0;
                     ss->pass = pass;
-                    if (!tmap_3d(&ss->tm_k, w.ks, (uint64_t)p->D, (uint64_t)Ns, (uint64_t)(p->B * p->Hkv),
+                    if (!tmap_3d(&ss->tm_k, level1 ? w.ks1 : w.ks, (uint64_t)p->D, (uint64_t)n, (uint64_t)(p->B * p->Hkv),
                                  (uint32_t)va::select_bn(epi)))
                         return cudaErrorInvalidValue;
                     return va::launch_select(*ss, epi, (int)p->D, cs);
                 };
-                if (e == cudaSuccess) e = run_sampled(va::EPI_TK_MINMAX, 0);
-                if (e == cudaSuccess) e = va::launch_tk_rows(sp, 1, kTkStride, cs);
+                if (e == cudaSuccess) e = run_sampled(va::EPI_TK_MINMAX, 0, true);
+                if (e == cudaSuccess) e = va::launch_tk_rows(sp, 1, kTkStride * kTkSub, cs);
                 if (e == cudaSuccess) e = cudaMemsetAsync(w.tk_hist, 0, (size_t)R * 256 * 4 * 2, cs);
-                if (e == cudaSuccess) e = run_sampled(va::EPI_TK_SHIST, 0);
-                if (e == cudaSuccess) e = va::launch_tk_rows(sp, 2, kTkStride, cs);
-                if (e == cudaSuccess) e = run_sampled(va::EPI_TK_SHIST, 1);
+                if (e == cudaSuccess) e = run_sampled(va::EPI_TK_SHIST, 0, true);
+                if (e == cudaSuccess) e = va::launch_tk_rows(sp, 2, kTkStride * kTkSub, cs);
+                if (e == cudaSuccess) e = run_sampled(va::EPI_TK_SHIST, 1, false);
                 if (e == cudaSuccess) e = va::launch_tk_rows(sp, 3, kTkStride, cs);
                 delete ss;
                 // VECATTN_TOPK_FORCE_FALLBACK=1 (tests): no candidate room -> every row takes the

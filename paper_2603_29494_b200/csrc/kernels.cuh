@@ -70,6 +70,8 @@ struct SelectParams {
     uint32_t* tk_fail;             // [R] 1: the window missed the k-th largest (fallback radix)
     int* tk_nfail;                 // rows with tk_fail
     float tk_sigma;                // window half-width in binomial sigmas of the sample rank (+8 ranks)
+    float tk_sigma1;               // level-1 range half-width (stride-64 sub-sample), binomial sigmas (+8)
+    uint32_t* tk_sabove;           // [R] stride-8 sampled scores above the level-2 range
     float alpha_raw[1024];         // per q head: alpha / scale (raw-accumulator units)
 };
 

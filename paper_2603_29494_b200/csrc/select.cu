@@ -434,12 +434,15 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
                 } else if constexpr (EPI == EPI_TK_SHIST) {
                     // bin = round((top - s) * invw): round-to-nearest by the 1.5*2^23 magic add,
                     // the integer read from the mantissa; bins outside [0, 255] are skipped
+                    // (level 2 also counts the scores above its range: bin < 0)
                     uint32_t* hcol = hist + r;
 #pragma unroll
                     for (int j = 0; j < 64; ++j) {
                         const float t = fmaf(v[j], -tk_b, tk_a) + 12582912.f;
-                        const uint32_t bin = (uint32_t)(__float_as_int(t) - 0x4B400000);
+                        const int bi = __float_as_int(t) - 0x4B400000;
+                        const uint32_t bin = (uint32_t)bi;
                         if (j < nvis && bin < 256u) atomicAdd(hcol + bin * 128, 1u);
+                        if (p.pass == 1) above += (j < nvis && bi < 0) ? 1u : 0u;
                     }
                 } else if constexpr (EPI == EPI_TK_CAND) {
                     // above = s > hi, inside = lo <= s <= hi, as sign bits of hi - s and s - lo
@@ -611,6 +614,7 @@ __global__ void __launch_bounds__(sel_threads<EPI>(), 1) select_kernel(const __g
                 if (above) atomicAdd(&p.tk_cabove[grow], above);
                 p.tk_ncand[grow * 2 * p.n_seg + slice] = ncand;
             } else if constexpr (EPI == EPI_TK_SHIST) {
+                if (above) atomicAdd(&p.tk_sabove[grow], above);
                 uint32_t* gh = p.tk_hist + ((int64_t)p.pass * p.BH * p.Np + grow) * 256;
                 if (p.n_seg == 1) {  // the whole sampled row in this unit: plain 16-B stores, half per warp set
                     for (int bin = 128 * eset; bin < 128 * eset + 128; bin += 4)
@@ -728,11 +732,12 @@ cudaError_t launch_topk_pick(const SelectParams& p, cudaStream_t st) {
 
 // ============================================================================ windowed TOPK
 // The radix TOPK above needs 4 histogram passes that touch every score (~10 ms each at dit128k).
-// Windowed TOPK: estimate the k-th largest score of each row from a 1-in-8 sample of the keys
-// (two cheap sampled passes: min/max, then a 256-bin histogram, refined once inside the bin
-// that holds the sample's k-th largest), take a window [lo, hi] around it wide enough for the
-// sampling error (6 sigma of the binomial rank), and make ONE full pass that counts the scores
-// above hi and collects those inside the window.  The exact k-th largest is then selected
+// Windowed TOPK: estimate the k-th largest score of each row from a 1-in-8 sample of the keys,
+// take a window [lo, hi] around it wide enough for the sampling error (c sigma of the binomial
+// rank), and make ONE full pass that counts the scores above hi and collects those inside the
+// window.  The sample ranks come from two histograms: level 1 (min/max, then 256 bins) on a
+// 1-in-64 sub-sample places the value range of level 2 (256 bins + a count of the scores above
+// it) on the 1-in-8 sample, wide enough (tk_sigma1 sub-sample sigmas) to hold the window.  The exact k-th largest is then selected
 // among the candidates; rows where the window missed it (or overflowed) fall back to the radix
 // passes.  The result (tk_prefix = order key of the k-th largest, tk_krem = ties to take) is
 // the same state the radix passes produce, so the emit pass and reading R12 are unchanged.
@@ -764,12 +769,13 @@ VA_DEV int64_t tk_budget(const SelectParams& p, int64_t vis_real) {  // k_i (rea
 }
 }  // namespace
 
-// stage 0: init; 1: level-1 binning over [smin, smax]; 2: level-2 binning inside the level-1
-// bin that holds the sample's k-th largest; 3: the window [lo, hi] from both histograms.
+// stage 0: init; 1: level-1 binning over [smin, smax] of the sub-sample; 2 (warp kernel below):
+// level-2 range = the level-1 bins holding the sub-sample ranks around the k-th largest;
+// 3 (warp kernel): the window [lo, hi] from the level-2 histogram and its above count.
 // Bin b of a level covers s with round((top - s) * invw) == b, i.e. s in [top - (b+.5)/invw,
 // top - (b-.5)/invw]; boundaries are widened by a relative 2^-16 (the exact counts of the
 // candidate pass decide, so a wider window only costs candidates).
-__global__ void __launch_bounds__(256) tk_rows_kernel(const __grid_constant__ SelectParams p, int stage, int stride) {
+__global__ void __launch_bounds__(256) tk_rows_kernel(const __grid_constant__ SelectParams p, int stage) {
     const int64_t R = p.BH * p.Np;
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= R) return;
@@ -778,96 +784,14 @@ __global__ void __launch_bounds__(256) tk_rows_kernel(const __grid_constant__ Se
         p.tk_smin[row] = 0xFFFFFFFFu;
         p.tk_fail[row] = 0u;
         p.tk_cabove[row] = 0u;
+        p.tk_sabove[row] = 0u;
         return;
     }
-    const int64_t i = row % p.Np;
-    const int64_t vis_real = p.causal ? min(p.N_real, (i + 1) * (int64_t)p.pq) : p.N_real;
-    const int64_t ns = (vis_real + stride - 1) / stride;  // visible sampled keys
+    // stage 1: level-1 binning over the sub-sample's [min, max]: bin = round((top - s) * invw)
     const float smax = f32_from_order_key(p.tk_smax[row]), smin = f32_from_order_key(p.tk_smin[row]);
-    if (stage == 1) {
-        const float w = smax - smin;
-        p.tk_top[row] = smax;
-        p.tk_invw[row] = w > 0.f ? 255.f / w : 0.f;
-        return;
-    }
-    const double ki = (double)tk_budget(p, vis_real);
-    const double ks = ki * (double)ns / (double)vis_real;  // the k-th largest's rank in the sample
-    const uint32_t* h1 = p.tk_hist + row * 256;
-    // level-1 binning (stage 1's, recomputed: tk_top / tk_invw hold level 2 after stage 2)
-    const float top1 = smax, invw1 = (smax - smin) > 0.f ? 255.f / (smax - smin) : 0.f;
-    // window ranks [ks - d, ks + d] in the sample, d = c sigma + 8 (binomial rank spread of a
-    // sample quantile; c = tk_sigma, 4.5 by default: measured |z| <= 3.5 over 48K rows,
-    // profiles/topk_window_r02.md; a missed row takes the exact radix fallback)
-    const double pr = min(1.0, ki / (double)vis_real);
-    const double d = (double)p.tk_sigma * sqrt((double)ns * pr * (1.0 - pr)) + 8.0;
-    const double r_lo = ks - d, r_hi = ks + d;
-    if (stage == 2) {
-        // level-1 bins ba..bb hold sample ranks r_lo..r_hi (counted from the top: bin 0 = the
-        // largest); level 2 re-bins exactly that value range into 256 sub-bins
-        double cum = 0.0;
-        int ba = -1, bb = 255;
-        for (int x = 0; x < 256; ++x) {
-            cum += h1[x];
-            if (ba < 0 && cum >= r_lo) ba = x;
-            if (cum >= r_hi) {
-                bb = x;
-                break;
-            }
-        }
-        if (ba < 0) ba = 255;
-        const float top2 = invw1 > 0.f ? top1 - ((float)ba - 0.5f) / invw1 : top1;
-        const float invw2 = invw1 > 0.f ? invw1 * 256.f / (float)(bb - ba + 1) : 0.f;
-        p.tk_lo[row] = (float)ba;  // stash the level-1 range for stage 3
-        p.tk_hi[row] = (float)bb;
-        p.tk_top[row] = top2;
-        p.tk_invw[row] = invw2;
-        return;
-    }
-    const int ba = (int)p.tk_lo[row], bb = (int)p.tk_hi[row];
-    const uint32_t* h2 = p.tk_hist + (R + row) * 256;
-    const float top2 = p.tk_top[row], invw2 = p.tk_invw[row];
-    // walk the sample from the top: level-1 bins < b, level-2 sub-bins of b, level-1 bins > b;
-    // hi = upper edge of the piece holding rank r_lo, lo = lower edge of the piece holding r_hi
-    float hi = INFINITY, lo = -INFINITY;
-    bool have_hi = r_lo < 1.0, have_lo = false;
-    double cum = 0.0;
-    auto visit = [&](double cnt, float upper, float lower) {
-        if (!have_hi && cum + cnt >= r_lo) {
-            hi = upper;
-            have_hi = true;
-        }
-        if (!have_lo && cum + cnt >= r_hi) {
-            lo = lower;
-            have_lo = true;
-        }
-        cum += cnt;
-    };
-    const bool flat = invw1 <= 0.f;
-    for (int x = 0; x < 256 && !have_lo; ++x) {
-        if (flat) {  // all sampled scores equal: one bin
-            visit((double)h1[x], top1, top1);
-            continue;
-        }
-        const float up1 = top1 - ((float)x - 0.5f) / invw1, dn1 = top1 - ((float)x + 0.5f) / invw1;
-        if (x < ba || x > bb) {
-            visit((double)h1[x], up1, dn1);
-        } else if (x == ba) {
-            // level-1 bins ba..bb as the 256 level-2 sub-bins; level-1 scores of the range that
-            // level 2 rounded out go half to each edge
-            double in1 = 0.0, in2 = 0.0;
-            for (int z = ba; z <= bb; ++z) in1 += h1[z];
-            for (int y = 0; y < 256; ++y) in2 += h2[y];
-            const double rest = in1 > in2 ? in1 - in2 : 0.0;
-            const float dnb = top1 - ((float)bb + 0.5f) / invw1;
-            visit(rest * 0.5, up1, up1);
-            for (int y = 0; y < 256 && !have_lo; ++y)
-                visit((double)h2[y], top2 - ((float)y - 0.5f) / invw2, top2 - ((float)y + 0.5f) / invw2);
-            visit(rest * 0.5, dnb, dnb);
-        }
-    }
-    const float e = 1.0f / 65536.0f;
-    p.tk_hi[row] = hi == INFINITY ? INFINITY : hi + fabsf(hi) * e + 1e-30f;
-    p.tk_lo[row] = lo == -INFINITY ? -INFINITY : lo - fabsf(lo) * e - 1e-30f;
+    const float w = smax - smin;
+    p.tk_top[row] = smax;
+    p.tk_invw[row] = w > 0.f ? 255.f / w : 0.f;
 }
 
 // Stages 2 and 3 of tk_rows_kernel with one warp per row: the histogram walks become warp
@@ -928,88 +852,51 @@ __global__ void __launch_bounds__(256) tk_rows_warp_kernel(const __grid_constant
     if (row >= R) return;
     const int64_t i = row % p.Np;
     const int64_t vis_real = p.causal ? min(p.N_real, (i + 1) * (int64_t)p.pq) : p.N_real;
-    const int64_t ns = (vis_real + stride - 1) / stride;
-    const float smax = f32_from_order_key(p.tk_smax[row]), smin = f32_from_order_key(p.tk_smin[row]);
+    const int64_t ns = (vis_real + stride - 1) / stride;  // visible keys of this sample
     const double ki = (double)tk_budget(p, vis_real);
-    const double ks = ki * (double)ns / (double)vis_real;
-    const uint32_t* h1 = p.tk_hist + row * 256;
-    const float top1 = smax, invw1 = (smax - smin) > 0.f ? 255.f / (smax - smin) : 0.f;
+    const double ks = ki * (double)ns / (double)vis_real;  // the k-th largest's rank in the sample
     const double pr = min(1.0, ki / (double)vis_real);
-    const double d = (double)p.tk_sigma * sqrt((double)ns * pr * (1.0 - pr)) + 8.0;
-    const double r_lo = ks - d, r_hi = ks + d;
+    const double sig = sqrt((double)ns * pr * (1.0 - pr));
     if (stage == 2) {
-        // doubled counts against doubled thresholds: the same first crossings as the thread walk
-        const TkScan sc = tk_warp_scan(h1, 0, 256, 0u, 2.0 * r_lo, 2.0 * r_hi, lane);
+        // sub-sample ranks [ks - d1, ks + d1], d1 = tk_sigma1 sigma + 8: wide enough that the
+        // values at the 1-in-8 sample's window ranks fall inside w.h.p. (both samples' errors)
+        const double d1 = (double)p.tk_sigma1 * sig + 8.0;
+        const uint32_t* h1 = p.tk_hist + row * 256;
+        const float smax = f32_from_order_key(p.tk_smax[row]), smin = f32_from_order_key(p.tk_smin[row]);
+        const float top1 = smax, invw1 = (smax - smin) > 0.f ? 255.f / (smax - smin) : 0.f;
+        // doubled counts against doubled thresholds (tk_warp_scan's convention)
+        const TkScan sc = tk_warp_scan(h1, 0, 256, 0u, 2.0 * (ks - d1), 2.0 * (ks + d1), lane);
         const int ba = sc.hit_lo < 0 ? 255 : sc.hit_lo;
         const int bb = sc.hit_hi < 0 ? 255 : sc.hit_hi;
         if (lane == 0) {
+            // level-2 range: level-1 bins ba..bb as 256 sub-bins (sub-bin 0 starts at bin ba's top)
             const float top2 = invw1 > 0.f ? top1 - ((float)ba - 0.5f) / invw1 : top1;
             const float invw2 = invw1 > 0.f ? invw1 * 256.f / (float)(bb - ba + 1) : 0.f;
-            p.tk_lo[row] = (float)ba;
-            p.tk_hi[row] = (float)bb;
             p.tk_top[row] = top2;
             p.tk_invw[row] = invw2;
         }
         return;
     }
-    const int ba = (int)p.tk_lo[row], bb = (int)p.tk_hi[row];
+    // stage 3: walk the 1-in-8 sample from the top: the scores above the level-2 range, then its
+    // 256 sub-bins; hi = upper edge of the piece holding rank r_lo, lo = lower edge of the piece
+    // holding r_hi (-inf when r_hi lies below the range, +inf when r_lo lies above it)
+    const double d = (double)p.tk_sigma * sig + 8.0;
+    const double r_lo = ks - d, r_hi = ks + d;
     const uint32_t* h2 = p.tk_hist + (R + row) * 256;
     const float top2 = p.tk_top[row], invw2 = p.tk_invw[row];
-    const double T_hi = 2.0 * r_lo, T_lo = 2.0 * r_hi;  // hi: where rank r_lo is reached; lo: r_hi
     float hi = INFINITY, lo = -INFINITY;
-    bool have_hi = r_lo < 1.0, have_lo = false;
-    uint32_t cum2 = 0;
-    // one segment of pieces: the first crossings give the edges (edge(x, upper?) of piece x)
-    auto seg = [&](const uint32_t* a, int s0, int n, auto up, auto dn) {
-        if (n <= 0 || have_lo) return;
-        const TkScan sc = tk_warp_scan(a, s0, n, cum2, T_hi, T_lo, lane);
-        if (!have_hi && sc.hit_lo >= 0) {
-            hi = up(sc.hit_lo);
-            have_hi = true;
+    if (invw2 > 0.f) {
+        const uint32_t ab2 = 2u * p.tk_sabove[row];
+        const double T_hi = 2.0 * r_lo, T_lo = 2.0 * r_hi;  // doubled counts
+        const bool hi_in_above = r_lo < 1.0 || (double)ab2 >= T_hi;
+        const bool lo_in_above = (double)ab2 >= T_lo;
+        if (lo_in_above) {
+            lo = top2 + 0.5f / invw2;  // the whole window lies above the range (hi = +inf)
+        } else {
+            const TkScan sc = tk_warp_scan(h2, 0, 256, ab2, T_hi, T_lo, lane);
+            if (!hi_in_above && sc.hit_lo >= 0) hi = top2 - ((float)sc.hit_lo - 0.5f) / invw2;
+            if (sc.hit_hi >= 0) lo = top2 - ((float)sc.hit_hi + 0.5f) / invw2;
         }
-        if (!have_lo && sc.hit_hi >= 0) {
-            lo = dn(sc.hit_hi);
-            have_lo = true;
-        }
-        cum2 += sc.total;
-    };
-    auto piece = [&](uint32_t cnt2, float edge) {  // one piece of doubled count cnt2
-        if (have_lo) return;
-        if (!have_hi && (double)(cum2 + cnt2) >= T_hi) {
-            hi = edge;
-            have_hi = true;
-        }
-        if ((double)(cum2 + cnt2) >= T_lo) {
-            lo = edge;
-            have_lo = true;
-        }
-        cum2 += cnt2;
-    };
-    if (invw1 <= 0.f) {  // all sampled scores equal: one bin
-        seg(h1, 0, 256, [&](int) { return top1; }, [&](int) { return top1; });
-    } else {
-        auto up1 = [&](int x) { return top1 - ((float)x - 0.5f) / invw1; };
-        auto dn1 = [&](int x) { return top1 - ((float)x + 0.5f) / invw1; };
-        seg(h1, 0, ba, up1, dn1);
-        // level-1 bins ba..bb as the 256 level-2 sub-bins; level-1 scores of the range that
-        // level 2 rounded out go half to each edge
-        uint32_t in1 = 0, in2 = 0;
-        for (int x = lane; x < 256; x += 32) {
-            in1 += (x >= ba && x <= bb) ? h1[x] : 0u;
-            in2 += h2[x];
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            in1 += __shfl_xor_sync(0xffffffffu, in1, o);
-            in2 += __shfl_xor_sync(0xffffffffu, in2, o);
-        }
-        const uint32_t rest = in1 > in2 ? in1 - in2 : 0u;  // doubled half = rest
-        const float dnb = top1 - ((float)bb + 0.5f) / invw1;
-        piece(rest, up1(ba));
-        seg(h2, 0, 256, [&](int y) { return top2 - ((float)y - 0.5f) / invw2; },
-            [&](int y) { return top2 - ((float)y + 0.5f) / invw2; });
-        piece(rest, dnb);
-        seg(h1, bb + 1, 255 - bb, [&](int x) { return up1(bb + 1 + x); }, [&](int x) { return dn1(bb + 1 + x); });
     }
     if (lane == 0) {
         const float e = 1.0f / 65536.0f;
@@ -1239,10 +1126,10 @@ cudaError_t launch_tk_sample_k(const void* k, void* ks, int64_t BHkv, int64_t N,
 cudaError_t launch_tk_rows(const SelectParams& p, int stage, int stride, cudaStream_t st) {
     const int64_t R = p.BH * p.Np;
     if (R <= 0) return cudaSuccess;
-    if (stage >= 2 && !getenv("VECATTN_TK_ROWS_THREAD"))  // (env: the thread-per-row walk, A/B only)
+    if (stage >= 2)
         tk_rows_warp_kernel<<<(unsigned)((R + 7) / 8), 256, 0, st>>>(p, stage, stride);
     else
-        tk_rows_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(p, stage, stride);
+        tk_rows_kernel<<<(unsigned)((R + 255) / 256), 256, 0, st>>>(p, stage);
     return cudaGetLastError();
 }
 

@@ -26,5 +26,9 @@ tot = []
 for name in runs[0]:
     ts = sorted(r.get(name, 0.0) for r in runs)
     print(f"{ts[1]:9.3f} ms  {name}")
+if os.environ.get("TOPK_PROF_ALL"):  # every launch of the last profiled call, in order
+    for e in prof.events():
+        if e.device_type.name == "CUDA":
+            print(f"   {e.device_time_total / 1000:9.3f} ms  {e.name[:70]}")
 tot = sorted(sum(r.values()) for r in runs)
 print(f"total {tot[1]:.3f} ms, nnz {int(off[-1])}")
