@@ -66,7 +66,9 @@ template <int kChunk, bool GATHER>
 VA_DEV Item decode_item(const AttnParams& p, int item) {
     Item I;
     I.bh = item / p.n_mt;
-    I.it = p.n_mt - 1 - (item % p.n_mt);  // longest-first within a head (causal)
+    // longest-first within a head: causal items by position (reversed), non-causal plans by
+    // their tile-chunk counts (p.item_order, written after the plan)
+    I.it = p.item_order != nullptr ? p.item_order[item] : p.n_mt - 1 - (item % p.n_mt);
     if constexpr (GATHER) {
         const int64_t G = 256 / p.pq;
         const int64_t x = I.bh * p.n_mt + I.it;

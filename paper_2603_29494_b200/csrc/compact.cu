@@ -281,6 +281,54 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const uint32_t* __re
     }
 }
 
+// ------------------------------------------------------------------- item order
+// One CTA per head: bitonic sort of the head's items by (tile-chunk count descending, item
+// ascending) in shared memory; order[bh*n_mt + pos] = the item at scheduler position pos.
+// Tile-chunks = 2 * chunks(both tiles) + chunks(tile 0) + chunks(tile 1), 64-key chunks.
+constexpr int kLptThreads = 1024;
+__global__ void __launch_bounds__(kLptThreads) lpt_order_kernel(const int32_t* __restrict__ wl_len, int64_t n_mt,
+                                                                int32_t* __restrict__ order) {
+    __shared__ unsigned long long key[kLptMaxItems];
+    const int64_t bh = blockIdx.x;
+    int n2 = 1;
+    while (n2 < n_mt) n2 <<= 1;
+    for (int i = threadIdx.x; i < n2; i += kLptThreads) {
+        unsigned long long k = ~0ull;  // padding sorts last
+        if (i < n_mt) {
+            const int32_t* l = wl_len + 3 * (bh * n_mt + i);
+            const uint32_t w = 2u * (uint32_t)((l[0] + 63) / 64) + (uint32_t)((l[1] + 63) / 64) +
+                               (uint32_t)((l[2] + 63) / 64);
+            k = ((unsigned long long)(0xFFFFFFFFu - w) << 32) | (uint32_t)i;
+        }
+        key[i] = k;
+    }
+    __syncthreads();
+    for (int size = 2; size <= n2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < n2; i += kLptThreads) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const unsigned long long a = key[i], b = key[j];
+                    if ((a > b) == up) {
+                        key[i] = b;
+                        key[j] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < n_mt; i += kLptThreads) order[bh * n_mt + i] = (int32_t)(key[i] & 0xFFFFFFFFull);
+}
+
+cudaError_t launch_lpt_order(const int32_t* wl_len, int64_t BH, int64_t n_mt, int32_t* order, cudaStream_t st) {
+    if (BH <= 0 || n_mt <= 0) return cudaSuccess;
+    if (n_mt > kLptMaxItems) return cudaErrorInvalidValue;
+    lpt_order_kernel<<<(unsigned)BH, kLptThreads, 0, st>>>(wl_len, n_mt, order);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_plan(const uint32_t* bitmask, int64_t words_per_row, const int64_t* offsets, const int64_t* d_nnz,
                         int64_t wl_cap, uint32_t* wl, int32_t* wl_len, int64_t BH, int64_t Np, int64_t N, int32_t pq,
                         int32_t causal, cudaStream_t st) {

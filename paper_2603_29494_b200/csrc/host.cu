@@ -825,10 +825,45 @@ vecattn_status_t vecattn_debug_scores(const vecattn_problem_t* p, int32_t pq, co
     return cuda_status(e);
 }
 
+// Longest-first item order within each head (non-causal plans): the dynamic
+// scheduler hands out a head's largest items first, so the step ends on its smallest ones.
+// VECATTN_ITEM_ORDER=0 keeps the position order (A/B knob).
+static cudaError_t item_order(AttnParams& ap, int32_t* order, cudaStream_t cs) {
+    static const bool off = [] {
+        const char* e = getenv("VECATTN_ITEM_ORDER");
+        return e != nullptr && e[0] == '0';
+    }();
+    ap.item_order = nullptr;
+    if (ap.causal || off || ap.n_mt > va::kLptMaxItems) return cudaSuccess;
+    ap.item_order = order;
+    return va::launch_lpt_order(ap.wl_len, ap.BH, ap.n_mt, order, cs);
+}
+
 size_t vecattn_sparse_workspace_bytes(const vecattn_problem_t* p, int32_t pq, int64_t nnz_cap) {
     if (check_problem(p) != VECATTN_OK || (pq != 64 && pq != 128) || nnz_cap < 0) return 0;
     const int64_t n_it = (p->N + 255) / 256;
-    return align_up((size_t)nnz_cap * 4) + align_up((size_t)(p->B * p->Hq * n_it) * 12) + kAlign;
+    return align_up((size_t)nnz_cap * 4) + align_up((size_t)(p->B * p->Hq * n_it) * 12) +
+           align_up((size_t)(p->B * p->Hq * n_it) * 4) + kAlign;
+}
+
+// Attention workspace: plan entries [nnz_cap], segment lengths [items][3], item order
+// [items] (per-head longest-first, non-causal), scheduler counters.
+struct AttnWs {
+    uint32_t* wl;
+    int32_t* wl_len;
+    int32_t* order;
+    int* counter;
+};
+static AttnWs carve_attn(uint8_t* b, int64_t nnz_cap, int64_t items) {
+    AttnWs w;
+    w.wl = reinterpret_cast<uint32_t*>(b);
+    b += align_up((size_t)nnz_cap * 4);
+    w.wl_len = reinterpret_cast<int32_t*>(b);
+    b += align_up((size_t)items * 12);
+    w.order = reinterpret_cast<int32_t*>(b);
+    b += align_up((size_t)items * 4);
+    w.counter = reinterpret_cast<int*>(b);
+    return w;
 }
 
 static vecattn_status_t attn_common(const vecattn_problem_t* p, const void* q, const void* k, const void* v,
@@ -884,10 +919,10 @@ vecattn_status_t vecattn_sparse_fwd(const vecattn_problem_t* p, int32_t pq, cons
                              !tmap_gather(&ap->tm_v, v, (uint64_t)p->D, (uint64_t)rows_kv)))
         st = VECATTN_ERR_UNSUPPORTED;
     if (st != VECATTN_OK) { delete ap; return st; }
-    uint8_t* b = static_cast<uint8_t*>(ws);
-    uint32_t* wl = reinterpret_cast<uint32_t*>(b);
-    int32_t* wl_len = reinterpret_cast<int32_t*>(b + align_up((size_t)nnz_cap * 4));
-    int* counter = reinterpret_cast<int*>(b + align_up((size_t)nnz_cap * 4) + align_up((size_t)(ap->BH * ap->n_mt) * 12));
+    const AttnWs aw = carve_attn(static_cast<uint8_t*>(ws), nnz_cap, ap->BH * ap->n_mt);
+    uint32_t* wl = aw.wl;
+    int32_t* wl_len = aw.wl_len;
+    int* counter = aw.counter;
     ap->Np = n_pooled(p, pq);
     ap->pq = pq;
     ap->wl = wl;
@@ -902,6 +937,7 @@ vecattn_status_t vecattn_sparse_fwd(const vecattn_problem_t* p, int32_t pq, cons
     tmark(1, cs);
     cudaError_t e = va::launch_worklist(offsets, indices ? indices : reinterpret_cast<const int32_t*>(wl), wl, wl_len,
                                         ap->BH, ap->Np, ap->n_mt, p->N, pq, nnz_cap, cs);
+    if (e == cudaSuccess) e = item_order(*ap, aw.order, cs);
     if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, 2 * sizeof(int), cs);
     tmark(2, cs);
     if (e == cudaSuccess) e = va::launch_attn(*ap, (int)p->D, true, attn_grid(ap->total_items), cs);
@@ -987,9 +1023,10 @@ vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_selec
                              !tmap_gather(&ap->tm_v, v, (uint64_t)p->D, (uint64_t)rows_kv)))
         st = VECATTN_ERR_UNSUPPORTED;
     if (st != VECATTN_OK) { delete sp; delete ap; return st; }
-    uint32_t* wl = reinterpret_cast<uint32_t*>(b);
-    int32_t* wl_len = reinterpret_cast<int32_t*>(b + align_up((size_t)nnz_cap * 4));
-    int* counter = reinterpret_cast<int*>(b + align_up((size_t)nnz_cap * 4) + align_up((size_t)(ap->BH * ap->n_mt) * 12));
+    const AttnWs aw = carve_attn(b, nnz_cap, ap->BH * ap->n_mt);
+    uint32_t* wl = aw.wl;
+    int32_t* wl_len = aw.wl_len;
+    int* counter = aw.counter;
     ap->Np = sp->Np;
     ap->pq = s->pq;
     ap->wl = wl;
@@ -1023,6 +1060,7 @@ vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_selec
     if (e == cudaSuccess)
         e = va::launch_plan(w.bitmask, sp->words_per_row, offsets, d_nnz, nnz_cap, wl, wl_len, sp->BH, sp->Np, p->N,
                             s->pq, p->causal ? 1 : 0, cs);
+    if (e == cudaSuccess) e = item_order(*ap, aw.order, cs);
     if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, 2 * sizeof(int), cs);
     tmark(2, cs);
     std::unique_lock<std::mutex> lk;

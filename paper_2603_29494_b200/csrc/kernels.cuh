@@ -146,6 +146,8 @@ struct AttnParams {
     int32_t pq, causal;
     float scale, scale_log2;
     int32_t strict_sync;           // attn_db: wait on every ODONE phase (compute-sanitizer synccheck runs)
+    const int32_t* item_order;     // gather, non-causal: [BH*n_mt] item within head for each scheduler
+                                   // position (per-head longest-first) or null (position order)
     int32_t die_mode;              // item scheduler: 0 one counter (head-major); 1/2 one counter per die
                                    // (die = smid < nsmid/2 / smid & 1), die d takes heads h = d (mod 2)
 };
@@ -155,6 +157,10 @@ cudaError_t launch_worklist(const int64_t* offsets, const int32_t* indices, uint
                             int64_t BH, int64_t Np, int64_t n_it, int64_t N, int32_t pq, int64_t cap,
                             cudaStream_t st);
 cudaError_t launch_attn(const AttnParams& p, int D, bool gather, int grid, cudaStream_t st);
+// Per-head longest-first order of the attention items by tile-chunk count (compact.cu):
+// order[bh*n_mt + pos] = item within head; one CTA per head, n_mt <= kLptMaxItems.
+constexpr int64_t kLptMaxItems = 2048;
+cudaError_t launch_lpt_order(const int32_t* wl_len, int64_t BH, int64_t n_mt, int32_t* order, cudaStream_t st);
 // Non-causal sparse attention on CTA pairs (attn_pair.cu, D = 128): grid = 2 x min(items, sms/2).
 int attn_pair_grid(int64_t items, int sms);
 cudaError_t launch_attn_pair(const AttnParams& p, int grid, cudaStream_t st);
