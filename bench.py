@@ -72,6 +72,9 @@ def parse():
     ap.add_argument("--quick", action="store_true", help="small debug run (no e2e/dense/cpu)")
     ap.add_argument("--no-context", action="store_true", help="skip the torch SDPA / flash-attn dense timings")
     ap.add_argument("--no-causal-extra", action="store_true", help="skip the causal vlm128k extra line")
+    ap.add_argument("--nccl-gather", action="store_true",
+                    help="N > 1: all-gather O with NCCL after each KV-head group instead of the fused "
+                         "symmetric-memory stores of the attention epilogue")
     return ap.parse_args()
 
 
@@ -172,6 +175,51 @@ class HeadGather:
                 n = self.B * (q1 - q0) * self.N * self.D
                 out[:, h0 + q0:h0 + q1] = self.recv[g][r, :n].view(self.B, q1 - q0, self.N, self.D)
         return out
+
+class SymmGather:
+    """C1 fused into the attention: the full O
+    [B, H, N, D] lives in torch symmetric memory on every rank, and each rank's attention
+    epilogue stores its heads' rows straight into every rank's buffer
+    (vecattn_forward_replicated: P2P stores over NVLink into the peers' mappings, or one NVLS
+    multicast store per row with VECATTN_NVLS=1 when the box exposes a multicast address).
+    No all-gather runs after the kernels, and uneven head splits need no padding.  A
+    symmetric-memory barrier before a step (every rank is done with the previous O) and after
+    it (every rank's stores have landed) orders the buffers.  `ok` is False (and `why` says
+    why) when symmetric memory is unavailable; the bench then uses HeadGather (NCCL)."""
+
+    def __init__(self, H, Hkv, B, N, D, ws, rank, dtype, device, ngroups=4, group=None):
+        self.H, self.B, self.N, self.D, self.ws, self.rank = H, B, N, D, ws, rank
+        self.plans = [kv_groups(H, Hkv, ws, r, ngroups) for r in range(ws)]
+        self.h0 = head_range(H, ws, rank)[0]
+        self.ok, self.why, self.mc, self.mode = False, "", 0, "p2p"
+        try:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+            self.buf = symm_mem.empty(B * H * N * D, dtype=dtype, device=device)
+            self.handle = symm_mem.rendezvous(self.buf, (group or dist.group.WORLD).group_name)
+            self.peers = [int(x) for x in self.handle.buffer_ptrs]
+            if os.environ.get("VECATTN_NVLS") == "1" and int(self.handle.multicast_ptr or 0):
+                self.mc, self.mode = int(self.handle.multicast_ptr), "nvls"
+            self.ok = len(self.peers) == ws and ws <= 8
+            if not self.ok:
+                self.why = f"{len(self.peers)} peer buffers for world size {ws}"
+        except Exception as e:  # no symmetric memory on this build / box
+            self.why = repr(e)
+
+    def run(self, compute):
+        """compute(g, (q0, q1, k0, k1), rep) runs the group's forward with replica `rep`."""
+        import paper_2603_29494_b200.vecattn as va
+        self.handle.barrier(channel=0)
+        for g, rng in enumerate(self.plans[self.rank]):
+            rep = va.replica([] if self.mc else self.peers, self.mc, self.h0 + rng[0], self.H)
+            compute(g, rng, rep)
+        self.handle.barrier(channel=0)
+
+    def bytes_received(self):
+        return self.buf.numel() * self.buf.element_size() * (self.ws - 1) // self.ws
+
+    def assemble(self):
+        return self.buf.view(self.B, self.H, self.N, self.D)
 
 # ------------------------------------------------------------------------- clocks
 class ClockSampler:
@@ -398,6 +446,10 @@ def run_ours(args):
     o = torch.empty_like(q)
     lse = torch.empty(B, Hl, N, dtype=torch.float32, device=dev)
     hg = HeadGather(H, Hkv, B, N, D, ws, rank, torch.bfloat16, dev) if ws > 1 else None
+    sg = SymmGather(H, Hkv, B, N, D, ws, rank, torch.bfloat16, dev) if ws > 1 and not args.nccl_gather else None
+    if sg is not None and not sg.ok:
+        print(f"[bench] symmetric memory unavailable ({sg.why}); NCCL all-gather instead", file=sys.stderr)
+        sg = None
     assert ws == 1 or B == 1, "head-group slices of [B,H,N,D] are contiguous only for B = 1"
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
@@ -406,6 +458,11 @@ def run_ours(args):
         q0, q1, k0, k1 = rng
         va.forward_into(q[:, q0:q1], k[:, k0:k1], v[:, k0:k1], cfg, offsets, indices, cap, d_nnz, cap, out,
                         lse[:, q0:q1], ws_fwd, causal)
+
+    def fwd_group_rep(g, rng, rep):
+        q0, q1, k0, k1 = rng
+        va.forward_replicated_into(q[:, q0:q1], k[:, k0:k1], v[:, k0:k1], cfg, offsets, indices, cap, d_nnz, cap,
+                                   None, lse[:, q0:q1], rep, ws_fwd, causal)
 
     def step(timers=None):
         """One hot-path pass: vecattn_forward (pool + select + CSR/plan + sparse attention);
@@ -416,6 +473,10 @@ def run_ours(args):
             ev[0].record(stream)
         if ws == 1:
             va.forward_into(q, k, v, cfg, offsets, indices, cap, d_nnz, cap, o, lse, ws_fwd, causal)
+            if ev:
+                ev[1].record(stream)
+        elif sg is not None:
+            sg.run(fwd_group_rep)
             if ev:
                 ev[1].record(stream)
         else:
@@ -654,11 +715,13 @@ def run_ours(args):
                    "pq": pq, "bk": bk, "gk": gk, "mode": args.mode, "alpha": alpha, "rho_target": args.rho,
                    "rho_achieved": round(1.0 - float(sp_tot[0]) / (4.0 * D) /
                                          (H * B * (N * N if not causal else N * (N + 1) / 2)), 5),
-                   "nnz": int(sp_tot[1]), "parallelism": f"head-parallel x{ws}" + (" + NCCL all-gather(O) per KV-head group, overlapped" if ws > 1 else ""),
+                   "nnz": int(sp_tot[1]), "parallelism": f"head-parallel x{ws}" + (
+                       "" if ws == 1 else (f" + O all-gather fused into the attention epilogue ({sg.mode} stores into symmetric memory)"
+                                           if sg is not None else " + NCCL all-gather(O) per KV-head group, overlapped")),
                    "l2": "256 MB L2 flush between timed steps; inputs (2.4 GB) >> L2"},
         "forward_ms": round(float(tt[1]) / args.steps, 4),
         "step_ms_warm_l2": round(warm_ms, 4),
-        "allgather_bytes_received_per_rank": hg.bytes_received() if ws > 1 else 0,
+        "allgather_bytes_received_per_rank": (sg or hg).bytes_received() if ws > 1 else 0,
         "breakdown_two_call": {"select_ms": round(sel_ms_avg, 4), "sparse_fwd_ms": round(sparse_ms_avg, 4),
                                "note": "vecattn_select + vecattn_sparse_fwd (CSR round trip), L2-flushed"},
         "dense_ms": round(dense_ms, 3) if dense_ms else None,

@@ -145,6 +145,40 @@ VECATTN_API vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const v
                                              void* o, float* lse, void* ws, size_t ws_bytes,
                                              vecattn_stream_t stream);
 
+/* ------------------------------------------- fused attention + all-gather */
+
+/* Output replication: the head-parallel output all-gather of the multi-GPU path (SURVEY
+ * 8(e) C1b) fused into the attention epilogue.  Every O row this call
+ * produces is stored straight into the full-size O buffer of every rank -- by P2P stores
+ * over NVLink into each peer's buffer (peer_o), or by one NVLS multicast store
+ * (multimem.st) when o_multicast is set -- instead of being all-gathered after the kernel.
+ * Row (b, h, r) of the call (h < p->Hq, the call's local query heads) lands at row
+ * ((b * heads_total + head0 + h) * N + r) of each [B, heads_total, N, D] bf16 buffer.
+ * The buffers are device addresses valid in the calling process (e.g. the peer mappings of a
+ * torch symmetric-memory allocation); they are written, never read.  The stores are weak:
+ * the caller orders them before any rank reads O (a cross-rank barrier after the call).
+ * Ownership stays with the caller; the library keeps no reference after the call.   */
+typedef struct {
+    int32_t n_peers;     /* 0..8 entries of peer_o (the caller's own buffer included)          */
+    void* peer_o[8];     /* 16-byte aligned device addresses of each rank's full O             */
+    void* o_multicast;   /* NVLS multicast address of the full O or NULL (then peer_o is used) */
+    int64_t head0;       /* first global query head of this call's heads, >= 0                 */
+    int64_t heads_total; /* query heads of the full O, >= head0 + p->Hq                         */
+} vecattn_replica_t;
+
+/* vecattn_forward with output replication.  `o` may be NULL (no local compact copy); if
+ * non-NULL it is written as by vecattn_forward.  rep == NULL or (n_peers == 0 and
+ * o_multicast == NULL) behaves exactly as vecattn_forward.  Errors: INVALID_ARGUMENT for
+ * n_peers outside 0..8, a NULL peer, head0 < 0 or head0 + p->Hq > heads_total, or o == NULL
+ * without a replica; SHAPE for a peer/multicast address not 16-byte aligned.  The CTA-pair
+ * kernel (VECATTN_PAIR=1) is not used when replicas are given.                         */
+VECATTN_API vecattn_status_t vecattn_forward_replicated(const vecattn_problem_t* p, const vecattn_select_params_t* s,
+                                                        const void* q, const void* k, const void* v,
+                                                        int64_t* offsets, int32_t* indices, int64_t cap,
+                                                        int64_t* d_nnz, int64_t nnz_cap, void* o, float* lse,
+                                                        const vecattn_replica_t* rep, void* ws, size_t ws_bytes,
+                                                        vecattn_stream_t stream);
+
 /* ------------------------------------------------------------- reference */
 
 VECATTN_API size_t vecattn_dense_workspace_bytes(const vecattn_problem_t* p);

@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
             // rows that only ever saw masked keys: l = 0 (non-members -> -2^100 -> 0), degenerate
             const float l = (m_ref < -0x1p99f * sl2) ? 0.f : lsum2.x + lsum2.y;  // scale-aware: masked = -2^100*sl2
             const float inv = l > 0.f ? 1.f / l : 0.f;
-            __nv_bfloat16* orow = p.o + (I.bh * p.N + qrow) * D;
+            const plan::ORow orow = plan::o_row<D>(p, I.bh, qrow);
             if (I.n_chunks > 0) {  // every MMA of the item complete (one OFIN phase per item with chunks)
                 mbar_wait(&bars[C::B_OFIN], fi & 1u);
                 ++fi;
@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                             w4.y = pack_bf16x2(__uint_as_float(ov[t + 2]) * inv, __uint_as_float(ov[t + 3]) * inv);
                             w4.z = pack_bf16x2(__uint_as_float(ov[t + 4]) * inv, __uint_as_float(ov[t + 5]) * inv);
                             w4.w = pack_bf16x2(__uint_as_float(ov[t + 6]) * inv, __uint_as_float(ov[t + 7]) * inv);
-                            __stcs(reinterpret_cast<uint4*>(orow + gq * 32 + t), w4);  // streamed: evict first
+                            plan::o_store16<D>(p, orow, gq * 32 + t, w4);  // streamed: evict first
                         }
                     }
                 }
@@ -623,10 +623,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     const __nv_bfloat16* kr = p.k + (bh_kv * p.N + qrow) * D;
                     const __nv_bfloat16* qr = p.q + (I.bh * p.N + qrow) * D;
                     float dot = 0.f;
-                    for (int t = 0; t < D; ++t) {
-                        orow[t] = vr[t];
-                        dot = fmaf(__bfloat162float(qr[t]), __bfloat162float(kr[t]), dot);
-                    }
+                    for (int t = 0; t < D; t += 8) plan::o_store16<D>(p, orow, t, *reinterpret_cast<const uint4*>(vr + t));
+                    for (int t = 0; t < D; ++t) dot = fmaf(__bfloat162float(qr[t]), __bfloat162float(kr[t]), dot);
                     if (p.lse) p.lse[I.bh * p.N + qrow] = dot * p.scale;
                 }
             }
@@ -846,7 +844,7 @@ static cudaError_t launch_attn_t(const AttnParams& p, int grid, cudaStream_t st)
 bool attn_uses_pair(const AttnParams& p, int D, bool gather) {
     // The CTA-pair kernel is correct but slower than the double-buffered single-SM kernel on
     // the dit128k plan (84 vs 74 ms, profiles/ubench_r02.md): opt-in with VECATTN_PAIR=1.
-    if (!gather || p.causal || D != 128) return false;
+    if (!gather || p.causal || D != 128 || p.rep_n > 0 || p.o_mc != nullptr) return false;
     const char* e = getenv("VECATTN_PAIR");
     return e != nullptr && e[0] == '1';
 }

@@ -613,7 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
             // rows that only ever saw masked keys carry m_ref ~ -2^100*scale*log2e: no visible key
             const float l = (m_ref < -0x1p99f * sl2) ? 0.f : lsum2.x + lsum2.y;  // scale-aware: masked = -2^100*sl2
             const float inv = l > 0.f ? 1.f / l : 0.f;
-            __nv_bfloat16* orow = p.o + (I.bh * p.N + qrow) * D;
+            const plan::ORow orow = plan::o_row<D>(p, I.bh, qrow);
             if (I.n_chunks > 0) {  // every PV of the item complete (ODONE parity may be 2 behind here)
                 mbar_wait(&bars[C::B_OFIN + tile], fi & 1u);
                 ++fi;
@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                             w.y = pack_bf16x2(__uint_as_float(ov[t + 2]) * inv, __uint_as_float(ov[t + 3]) * inv);
                             w.z = pack_bf16x2(__uint_as_float(ov[t + 4]) * inv, __uint_as_float(ov[t + 5]) * inv);
                             w.w = pack_bf16x2(__uint_as_float(ov[t + 6]) * inv, __uint_as_float(ov[t + 7]) * inv);
-                            __stcs(reinterpret_cast<uint4*>(orow + g * 32 + t), w);  // streamed: evict first
+                            plan::o_store16<D>(p, orow, g * 32 + t, w);  // streamed: evict first
                         }
                     }
                 }
@@ -654,10 +654,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                     const __nv_bfloat16* kr = p.k + (bh_kv * p.N + qrow) * D;
                     const __nv_bfloat16* qr = p.q + (I.bh * p.N + qrow) * D;
                     float dot = 0.f;
-                    for (int t = 0; t < D; ++t) {
-                        orow[t] = vr[t];
-                        dot = fmaf(__bfloat162float(qr[t]), __bfloat162float(kr[t]), dot);
-                    }
+                    for (int t = 0; t < D; t += 8) plan::o_store16<D>(p, orow, t, *reinterpret_cast<const uint4*>(vr + t));
+                    for (int t = 0; t < D; ++t) dot = fmaf(__bfloat162float(qr[t]), __bfloat162float(kr[t]), dot);
                     if (p.lse) p.lse[I.bh * p.N + qrow] = dot * p.scale;
                 }
             }

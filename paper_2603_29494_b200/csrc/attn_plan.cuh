@@ -156,5 +156,37 @@ VA_DEV int next_chunk(const Item& I, int t, int j) {
     }
 }
 
+// ---------------------------------------------------------------- O output
+// An O row goes to the call's own buffer (p.o, may be null) and, for the fused all-gather
+// (vecattn_forward_replicated), to the same row of every rank's full O:
+// P2P stores into each peer's buffer, or one multimem (NVLS multicast) store.
+struct ORow {
+    __nv_bfloat16* local;  // this row in p.o, or null
+    int64_t grow;          // row index in the replica buffers
+};
+template <int D>
+VA_DEV ORow o_row(const AttnParams& p, int64_t bh, int64_t qrow) {
+    ORow r;
+    r.local = p.o != nullptr ? p.o + (bh * p.N + qrow) * D : nullptr;
+    const int64_t b = bh / p.Hq, h = bh % p.Hq;
+    r.grow = (b * p.rep_heads + p.rep_head0 + h) * p.N + qrow;
+    return r;
+}
+VA_DEV void multimem_st16(void* addr, uint4 w) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "r"(w.x), "r"(w.y),
+                 "r"(w.z), "r"(w.w)
+                 : "memory");
+}
+// 16 bytes (8 bf16) of row r at column col; streamed (evict-first) stores
+template <int D>
+VA_DEV void o_store16(const AttnParams& p, const ORow& r, int col, uint4 w) {
+    if (r.local != nullptr) __stcs(reinterpret_cast<uint4*>(r.local + col), w);
+    if (p.o_mc != nullptr) {
+        multimem_st16(p.o_mc + r.grow * D + col, w);
+    } else {
+        for (int i = 0; i < p.rep_n; ++i) __stcs(reinterpret_cast<uint4*>(p.rep_o[i] + r.grow * D + col), w);
+    }
+}
+
 }  // namespace plan
 }  // namespace va

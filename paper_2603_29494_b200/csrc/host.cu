@@ -999,15 +999,27 @@ size_t vecattn_forward_workspace_bytes(const vecattn_problem_t* p, const vecattn
     return carve_select(p, s->pq, nullptr, s->mode == VECATTN_SEL_TOPK).total + vecattn_sparse_workspace_bytes(p, s->pq, nnz_cap);
 }
 
-vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_select_params_t* s, const void* q,
-                                 const void* k, const void* v, int64_t* offsets, int32_t* indices, int64_t cap,
-                                 int64_t* d_nnz, int64_t nnz_cap, void* o, float* lse, void* ws, size_t ws_bytes,
-                                 vecattn_stream_t stream) {
+static vecattn_status_t forward_impl(const vecattn_problem_t* p, const vecattn_select_params_t* s, const void* q,
+                                     const void* k, const void* v, int64_t* offsets, int32_t* indices, int64_t cap,
+                                     int64_t* d_nnz, int64_t nnz_cap, void* o, float* lse,
+                                     const vecattn_replica_t* rep, void* ws, size_t ws_bytes,
+                                     vecattn_stream_t stream) {
     vecattn_status_t st = check_select(p, s);
     if (st != VECATTN_OK) return st;
-    if (!q || !k || !v || !o || !offsets || !d_nnz || cap < 0 || (cap > 0 && !indices) || nnz_cap < 0)
+    const bool replicate = rep != nullptr && (rep->n_peers > 0 || rep->o_multicast != nullptr);
+    if (!q || !k || !v || (!o && !replicate) || !offsets || !d_nnz || cap < 0 || (cap > 0 && !indices) ||
+        nnz_cap < 0)
         return VECATTN_ERR_INVALID_ARGUMENT;
-    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o)) return VECATTN_ERR_SHAPE;
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || (o && !aligned16(o))) return VECATTN_ERR_SHAPE;
+    if (rep != nullptr) {
+        if (rep->n_peers < 0 || rep->n_peers > 8 || rep->head0 < 0 || rep->head0 + p->Hq > rep->heads_total)
+            return VECATTN_ERR_INVALID_ARGUMENT;
+        for (int i = 0; i < rep->n_peers && rep->o_multicast == nullptr; ++i) {
+            if (!rep->peer_o[i]) return VECATTN_ERR_INVALID_ARGUMENT;
+            if (!aligned16(rep->peer_o[i])) return VECATTN_ERR_SHAPE;
+        }
+        if (rep->o_multicast && !aligned16(rep->o_multicast)) return VECATTN_ERR_SHAPE;
+    }
     const size_t need = vecattn_forward_workspace_bytes(p, s, nnz_cap);
     if (!ws || ws_bytes < need) return VECATTN_ERR_WORKSPACE;
     if (!aligned16(ws)) return VECATTN_ERR_SHAPE;
@@ -1023,6 +1035,13 @@ vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_selec
                              !tmap_gather(&ap->tm_v, v, (uint64_t)p->D, (uint64_t)rows_kv)))
         st = VECATTN_ERR_UNSUPPORTED;
     if (st != VECATTN_OK) { delete sp; delete ap; return st; }
+    if (replicate) {
+        ap->o_mc = static_cast<__nv_bfloat16*>(rep->o_multicast);
+        ap->rep_n = rep->o_multicast ? 0 : rep->n_peers;
+        for (int i = 0; i < ap->rep_n; ++i) ap->rep_o[i] = static_cast<__nv_bfloat16*>(rep->peer_o[i]);
+        ap->rep_head0 = rep->head0;
+        ap->rep_heads = rep->heads_total;
+    }
     const AttnWs aw = carve_attn(b, nnz_cap, ap->BH * ap->n_mt);
     uint32_t* wl = aw.wl;
     int32_t* wl_len = aw.wl_len;
@@ -1081,6 +1100,21 @@ vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_selec
     delete sp;
     delete ap;
     return cuda_status(e);
+}
+
+vecattn_status_t vecattn_forward(const vecattn_problem_t* p, const vecattn_select_params_t* s, const void* q,
+                                 const void* k, const void* v, int64_t* offsets, int32_t* indices, int64_t cap,
+                                 int64_t* d_nnz, int64_t nnz_cap, void* o, float* lse, void* ws, size_t ws_bytes,
+                                 vecattn_stream_t stream) {
+    return forward_impl(p, s, q, k, v, offsets, indices, cap, d_nnz, nnz_cap, o, lse, nullptr, ws, ws_bytes, stream);
+}
+
+vecattn_status_t vecattn_forward_replicated(const vecattn_problem_t* p, const vecattn_select_params_t* s,
+                                            const void* q, const void* k, const void* v, int64_t* offsets,
+                                            int32_t* indices, int64_t cap, int64_t* d_nnz, int64_t nnz_cap, void* o,
+                                            float* lse, const vecattn_replica_t* rep, void* ws, size_t ws_bytes,
+                                            vecattn_stream_t stream) {
+    return forward_impl(p, s, q, k, v, offsets, indices, cap, d_nnz, nnz_cap, o, lse, rep, ws, ws_bytes, stream);
 }
 
 }  // extern "C"

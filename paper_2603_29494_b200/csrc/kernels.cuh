@@ -148,6 +148,12 @@ struct AttnParams {
     int32_t strict_sync;           // attn_db: wait on every ODONE phase (compute-sanitizer synccheck runs)
     const int32_t* item_order;     // gather, non-causal: [BH*n_mt] item within head for each scheduler
                                    // position (per-head longest-first) or null (position order)
+    // output replication (vecattn_forward_replicated): each O row also goes to row
+    // ((b*rep_heads + rep_head0 + h)*N + r) of every rep_o[i], or once to o_mc (NVLS multicast)
+    __nv_bfloat16* rep_o[8];
+    __nv_bfloat16* o_mc;
+    int64_t rep_head0, rep_heads;
+    int32_t rep_n;
     int32_t die_mode;              // item scheduler: 0 one counter (head-major); 1/2 one counter per die
                                    // (die = smid < nsmid/2 / smid & 1), die d takes heads h = d (mod 2)
 };
@@ -166,7 +172,7 @@ int attn_pair_grid(int64_t items, int sms);
 cudaError_t launch_attn_pair(const AttnParams& p, int grid, cudaStream_t st);
 int grid_sms();  // SM count of the current device
 // true if launch_attn runs the pair kernel for this problem (it fills its SMs: no side CTA fits)
-bool attn_uses_pair(const AttnParams& p, int D, bool gather);
+bool attn_uses_pair(const AttnParams& p, int D, bool gather);  // false when replicas are given
 // Double-buffered 64-key variant of the gather kernel (attn_db.cu), used for non-causal plans.
 cudaError_t launch_attn_db(const AttnParams& p, int D, int grid, cudaStream_t st);
 

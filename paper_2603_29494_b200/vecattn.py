@@ -41,6 +41,12 @@ class SelectParams(ctypes.Structure):
                 ("topk", ctypes.c_int64), ("keep_frac", ctypes.c_float)]
 
 
+class Replica(ctypes.Structure):
+    """vecattn_replica_t (include/vecattn.h): where the fused attention -> all-gather stores O."""
+    _fields_ = [("n_peers", ctypes.c_int32), ("peer_o", ctypes.c_void_p * 8), ("o_multicast", ctypes.c_void_p),
+                ("head0", ctypes.c_int64), ("heads_total", ctypes.c_int64)]
+
+
 _lib = None
 
 
@@ -65,6 +71,8 @@ def load(path: str = LIB_PATH):
         "vecattn_dense_fwd": (i32, [prob, vp, vp, vp, vp, vp, vp, sz, vp]),
         "vecattn_forward_workspace_bytes": (sz, [prob, sel, i64]),
         "vecattn_forward": (i32, [prob, sel, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp, vp, sz, vp]),
+        "vecattn_forward_replicated": (i32, [prob, sel, vp, vp, vp, vp, vp, i64, vp, i64, vp, vp, P(Replica), vp, sz,
+                                             vp]),
         "vecattn_validate_selection": (i32, [prob, i32, vp, vp, vp, vp]),
         "vecattn_debug_scores": (i32, [prob, i32, vp, vp, vp, vp, sz, vp]),
         "vecattn_status_string": (ctypes.c_char_p, [i32]),
@@ -88,7 +96,7 @@ def load(path: str = LIB_PATH):
 
 EXPORTED = ["vecattn_pool", "vecattn_select_workspace_bytes", "vecattn_select", "vecattn_sparse_workspace_bytes",
             "vecattn_sparse_fwd", "vecattn_dense_workspace_bytes", "vecattn_dense_fwd",
-            "vecattn_forward_workspace_bytes", "vecattn_forward",
+            "vecattn_forward_workspace_bytes", "vecattn_forward", "vecattn_forward_replicated",
             "vecattn_validate_selection", "vecattn_debug_scores", "vecattn_status_string", "vecattn_last_cuda_error",
             "vecattn_abi_version", "vecattn_kernel_timing", "vecattn_kernel_timing_last",
             "vecattn_select_naive_workspace_bytes", "vecattn_select_naive", "vecattn_alpha_dp"]
@@ -405,6 +413,39 @@ def forward_into(q, k, v, cfg: SelectConfig, offsets, indices, cap: int, d_nnz, 
                              _ptr(indices), int(cap), _ptr(d_nnz), int(nnz_cap), _ptr(o), _ptr(lse), _ptr(ws),
                              ws.numel(), _stream(stream))
     _check("vecattn_forward", rc)
+
+
+def replica(peer_ptrs=(), multicast_ptr: int = 0, head0: int = 0, heads_total: int = 0) -> Replica:
+    """vecattn_replica_t from raw device addresses (e.g. a torch symmetric-memory handle's
+    buffer_ptrs / multicast_ptr) of every rank's full O [B, heads_total, N, D] bf16."""
+    peer_ptrs = [int(x) for x in peer_ptrs]
+    if len(peer_ptrs) > 8:
+        raise ValueError("vecattn: at most 8 replicas")
+    r = Replica()
+    r.n_peers = len(peer_ptrs)
+    for i, x in enumerate(peer_ptrs):
+        r.peer_o[i] = x
+    r.o_multicast = int(multicast_ptr) or None
+    r.head0 = int(head0)
+    r.heads_total = int(heads_total)
+    return r
+
+
+def forward_replicated_into(q, k, v, cfg: SelectConfig, offsets, indices, cap: int, d_nnz, nnz_cap: int, o, lse,
+                            rep: Replica, ws: torch.Tensor, causal: bool, scale=None, stream=None):
+    """Raw vecattn_forward_replicated: vecattn_forward whose attention epilogue also stores
+    every O row into each replica buffer (the fused output all-gather).  o may be None."""
+    lib = load()
+    _dev_check(q, k, v, offsets, indices, d_nnz, o, lse)
+    _check_io(q, k, v, o, lse, offsets=offsets, indices=indices, d_nnz=d_nnz, pq=cfg.pq, cfg=cfg)
+    if indices is not None and indices.numel() < cap:
+        raise ValueError(f"vecattn: indices has {indices.numel()} entries < cap={cap}")
+    pr = problem(q, k, causal, scale)
+    sp = cfg.params()
+    rc = lib.vecattn_forward_replicated(ctypes.byref(pr), ctypes.byref(sp), _ptr(q), _ptr(k), _ptr(v), _ptr(offsets),
+                                        _ptr(indices), int(cap), _ptr(d_nnz), int(nnz_cap), _ptr(o), _ptr(lse),
+                                        ctypes.byref(rep), _ptr(ws), ws.numel(), _stream(stream))
+    _check("vecattn_forward_replicated", rc)
 
 
 def forward(q, k, v, cfg: SelectConfig, causal: bool = False, scale=None, nnz_cap: int | None = None,
