@@ -829,12 +829,12 @@ vecattn_status_t vecattn_debug_scores(const vecattn_problem_t* p, int32_t pq, co
 // scheduler hands out a head's largest items first, so the step ends on its smallest ones.
 // VECATTN_ITEM_ORDER=0 keeps the position order (A/B knob).
 static cudaError_t item_order(AttnParams& ap, int32_t* order, cudaStream_t cs) {
-    static const bool off = [] {
+    static const int mode = [] {  // 0 position order, 1 non-causal only (default), 2 causal too
         const char* e = getenv("VECATTN_ITEM_ORDER");
-        return e != nullptr && e[0] == '0';
+        return e == nullptr ? 1 : atoi(e);
     }();
     ap.item_order = nullptr;
-    if (ap.causal || off || ap.n_mt > va::kLptMaxItems) return cudaSuccess;
+    if ((ap.causal && mode < 2) || mode == 0 || ap.n_mt > va::kLptMaxItems) return cudaSuccess;
     ap.item_order = order;
     return va::launch_lpt_order(ap.wl_len, ap.BH, ap.n_mt, order, cs);
 }
