@@ -189,7 +189,9 @@ class SymmGather:
 
     def __init__(self, H, Hkv, B, N, D, ws, rank, dtype, device, ngroups=4, group=None):
         self.H, self.B, self.N, self.D, self.ws, self.rank = H, B, N, D, ws, rank
-        self.plans = [kv_groups(H, Hkv, ws, r, ngroups) for r in range(ws)]
+        # one call over all local heads: there is no all-gather to overlap with later groups,
+        # and one call gives the attention's item scheduler the whole rank's items to balance
+        self.plans = [kv_groups(H, Hkv, ws, r, 1) for r in range(ws)]
         self.h0 = head_range(H, ws, rank)[0]
         self.ok, self.why, self.mc, self.mode = False, "", 0, "p2p"
         try:
