@@ -449,9 +449,13 @@ def run_ours(args):
     lse = torch.empty(B, Hl, N, dtype=torch.float32, device=dev)
     hg = HeadGather(H, Hkv, B, N, D, ws, rank, torch.bfloat16, dev) if ws > 1 else None
     sg = SymmGather(H, Hkv, B, N, D, ws, rank, torch.bfloat16, dev) if ws > 1 and not args.nccl_gather else None
-    if sg is not None and not sg.ok:
-        print(f"[bench] symmetric memory unavailable ({sg.why}); NCCL all-gather instead", file=sys.stderr)
-        sg = None
+    if sg is not None:
+        okt = torch.tensor([1 if sg.ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)  # every rank takes the same all-gather path
+        if not int(okt.item()):
+            print(f"[bench] symmetric memory unavailable ({sg.why or 'on another rank'}); NCCL all-gather instead",
+                  file=sys.stderr)
+            sg = None
     assert ws == 1 or B == 1, "head-group slices of [B,H,N,D] are contiguous only for B = 1"
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
