@@ -264,10 +264,17 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const uint32_t* __re
             }
         }
         __syncthreads();
-        const int rsum = rt0 + rt1 + rt2;
-        for (int t = tid; t < rsum; t += kPlanThreads) {
-            const int64_t dst = t < rt0 ? run[0] + t : (t < rt0 + rt1 ? run[1] + (t - rt0) : run[2] + (t - rt0 - rt1));
-            wl[dst] = stage[t];
+        // one coalesced copy loop per segment (pointer-stepped: fewer instructions per entry than
+        // one loop that picks the segment of every entry)
+        {
+            uint32_t* d0 = wl + run[0];
+            for (int t = tid; t < rt0; t += kPlanThreads) d0[t] = stage[t];
+            uint32_t* d1 = wl + run[1];
+            const uint32_t* s1 = stage + rt0;
+            for (int t = tid; t < rt1; t += kPlanThreads) d1[t] = s1[t];
+            uint32_t* d2 = wl + run[2];
+            const uint32_t* s2 = stage + rt0 + rt1;
+            for (int t = tid; t < rt2; t += kPlanThreads) d2[t] = s2[t];
         }
         run[0] += rt0;
         run[1] += rt1;
