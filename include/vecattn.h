@@ -164,14 +164,22 @@ typedef struct {
     void* o_multicast;   /* NVLS multicast address of the full O or NULL (then peer_o is used) */
     int64_t head0;       /* first global query head of this call's heads, >= 0                 */
     int64_t heads_total; /* query heads of the full O, >= head0 + p->Hq                         */
+    int64_t item_begin;  /* work window over the call's 256-row attention items, flattened as  */
+    int64_t item_end;    /* (b*Hq + h) * ceil(N/256) + r/256: only rows of items in            */
+                         /* [item_begin, item_end) are computed and stored (O, replicas, LSE); */
+                         /* item_end <= 0 = every item.  The selection (offsets/indices) still */
+                         /* covers every row of the call.                                       */
 } vecattn_replica_t;
 
 /* vecattn_forward with output replication.  `o` may be NULL (no local compact copy); if
  * non-NULL it is written as by vecattn_forward.  rep == NULL or (n_peers == 0 and
  * o_multicast == NULL) behaves exactly as vecattn_forward.  Errors: INVALID_ARGUMENT for
- * n_peers outside 0..8, a NULL peer, head0 < 0 or head0 + p->Hq > heads_total, or o == NULL
- * without a replica; SHAPE for a peer/multicast address not 16-byte aligned.  The CTA-pair
- * kernel (VECATTN_PAIR=1) is not used when replicas are given.                         */
+ * n_peers outside 0..8, a NULL peer, head0 < 0 or head0 + p->Hq > heads_total, a work
+ * window outside [0, B*Hq*ceil(N/256)] or empty, or o == NULL without a replica; SHAPE for a
+ * peer/multicast address not 16-byte aligned.  The work window is the flattened (head, block)
+ * partition of SURVEY 8(e): ranks split B*H*ceil(N/256) items evenly, each calling with the
+ * heads its window touches.  The CTA-pair kernel (VECATTN_PAIR=1) is not used with replicas
+ * or windows.                                                                           */
 VECATTN_API vecattn_status_t vecattn_forward_replicated(const vecattn_problem_t* p, const vecattn_select_params_t* s,
                                                         const void* q, const void* k, const void* v,
                                                         int64_t* offsets, int32_t* indices, int64_t cap,

@@ -844,7 +844,8 @@ static cudaError_t launch_attn_t(const AttnParams& p, int grid, cudaStream_t st)
 bool attn_uses_pair(const AttnParams& p, int D, bool gather) {
     // The CTA-pair kernel is correct but slower than the double-buffered single-SM kernel on
     // the dit128k plan (84 vs 74 ms, profiles/ubench_r02.md): opt-in with VECATTN_PAIR=1.
-    if (!gather || p.causal || D != 128 || p.rep_n > 0 || p.o_mc != nullptr) return false;
+    if (!gather || p.causal || D != 128 || p.rep_n > 0 || p.o_mc != nullptr || p.total_items != p.BH * p.n_mt)
+        return false;
     const char* e = getenv("VECATTN_PAIR");
     return e != nullptr && e[0] == '1';
 }

@@ -65,10 +65,13 @@ struct Chunk {
 template <int kChunk, bool GATHER>
 VA_DEV Item decode_item(const AttnParams& p, int item) {
     Item I;
-    I.bh = item / p.n_mt;
-    // longest-first within a head: causal items by position (reversed), non-causal plans by
-    // their tile-chunk counts (p.item_order, written after the plan)
-    I.it = p.item_order != nullptr ? p.item_order[item] : p.n_mt - 1 - (item % p.n_mt);
+    // scheduler position -> item (bh * n_mt + it).  Longest-first within a head: causal items
+    // by position (reversed); with p.item_order (written after the plan), non-causal plans by
+    // their tile-chunk counts, and work windows (vecattn_replica_t) over the window's items.
+    const int64_t x = p.item_order != nullptr ? (int64_t)p.item_order[item]
+                                              : (item / p.n_mt) * p.n_mt + (p.n_mt - 1 - (item % p.n_mt));
+    I.bh = x / p.n_mt;
+    I.it = x % p.n_mt;
     if constexpr (GATHER) {
         const int64_t G = 256 / p.pq;
         const int64_t x = I.bh * p.n_mt + I.it;

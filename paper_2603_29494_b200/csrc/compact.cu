@@ -289,23 +289,40 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const uint32_t* __re
 }
 
 // ------------------------------------------------------------------- item order
-// One CTA per head: bitonic sort of the head's items by (tile-chunk count descending, item
-// ascending) in shared memory; order[bh*n_mt + pos] = the item at scheduler position pos.
-// Tile-chunks = 2 * chunks(both tiles) + chunks(tile 0) + chunks(tile 1), 64-key chunks.
+// One CTA per head: the head's items inside the window [lo, hi) of the flattened items, sorted
+// in shared memory (bitonic) by (weight descending, item ascending) -- weight = tile-chunks
+// 2 * chunks(both tiles) + chunks(tile 0) + chunks(tile 1) of 64 keys, or (by_position, the
+// causal default: later items see more keys) the item's position -- and written at the head's
+// offset in the window: order[pos] = bh * n_mt + it.
 constexpr int kLptThreads = 1024;
 __global__ void __launch_bounds__(kLptThreads) lpt_order_kernel(const int32_t* __restrict__ wl_len, int64_t n_mt,
+                                                                int64_t lo, int64_t hi, int32_t by_position,
                                                                 int32_t* __restrict__ order) {
     __shared__ unsigned long long key[kLptMaxItems];
     const int64_t bh = blockIdx.x;
+    const int64_t h0 = bh * n_mt;
+    const int64_t a = max(lo, h0) - h0, b = min(hi, h0 + n_mt) - h0;  // items [a, b) of this head
+    if (b <= a) return;
+    const int64_t n = b - a;
+    int32_t* out = order + (max(lo, h0) - lo);
+    if (n_mt > kLptMaxItems) {  // position order, reversed (longest first when causal)
+        for (int64_t i = threadIdx.x; i < n; i += kLptThreads) out[i] = (int32_t)(h0 + b - 1 - i);
+        return;
+    }
     int n2 = 1;
-    while (n2 < n_mt) n2 <<= 1;
+    while (n2 < n) n2 <<= 1;
     for (int i = threadIdx.x; i < n2; i += kLptThreads) {
         unsigned long long k = ~0ull;  // padding sorts last
-        if (i < n_mt) {
-            const int32_t* l = wl_len + 3 * (bh * n_mt + i);
-            const uint32_t w = 2u * (uint32_t)((l[0] + 63) / 64) + (uint32_t)((l[1] + 63) / 64) +
-                               (uint32_t)((l[2] + 63) / 64);
-            k = ((unsigned long long)(0xFFFFFFFFu - w) << 32) | (uint32_t)i;
+        if (i < n) {
+            const int64_t it = a + i;
+            uint32_t w;
+            if (by_position) {
+                w = (uint32_t)it;
+            } else {
+                const int32_t* l = wl_len + 3 * (h0 + it);
+                w = 2u * (uint32_t)((l[0] + 63) / 64) + (uint32_t)((l[1] + 63) / 64) + (uint32_t)((l[2] + 63) / 64);
+            }
+            k = ((unsigned long long)(0xFFFFFFFFu - w) << 32) | (uint32_t)it;
         }
         key[i] = k;
     }
@@ -316,23 +333,23 @@ __global__ void __launch_bounds__(kLptThreads) lpt_order_kernel(const int32_t* _
                 const int j = i ^ stride;
                 if (j > i) {
                     const bool up = (i & size) == 0;
-                    const unsigned long long a = key[i], b = key[j];
-                    if ((a > b) == up) {
-                        key[i] = b;
-                        key[j] = a;
+                    const unsigned long long x = key[i], y = key[j];
+                    if ((x > y) == up) {
+                        key[i] = y;
+                        key[j] = x;
                     }
                 }
             }
             __syncthreads();
         }
     }
-    for (int i = threadIdx.x; i < n_mt; i += kLptThreads) order[bh * n_mt + i] = (int32_t)(key[i] & 0xFFFFFFFFull);
+    for (int i = threadIdx.x; i < n; i += kLptThreads) out[i] = (int32_t)(h0 + (int64_t)(key[i] & 0xFFFFFFFFull));
 }
 
-cudaError_t launch_lpt_order(const int32_t* wl_len, int64_t BH, int64_t n_mt, int32_t* order, cudaStream_t st) {
-    if (BH <= 0 || n_mt <= 0) return cudaSuccess;
-    if (n_mt > kLptMaxItems) return cudaErrorInvalidValue;
-    lpt_order_kernel<<<(unsigned)BH, kLptThreads, 0, st>>>(wl_len, n_mt, order);
+cudaError_t launch_lpt_order(const int32_t* wl_len, int64_t BH, int64_t n_mt, int64_t lo, int64_t hi,
+                             int32_t by_position, int32_t* order, cudaStream_t st) {
+    if (BH <= 0 || n_mt <= 0 || hi <= lo) return cudaSuccess;
+    lpt_order_kernel<<<(unsigned)BH, kLptThreads, 0, st>>>(wl_len, n_mt, lo, hi, by_position, order);
     return cudaGetLastError();
 }
 

@@ -828,15 +828,21 @@ vecattn_status_t vecattn_debug_scores(const vecattn_problem_t* p, int32_t pq, co
 // Longest-first item order within each head (non-causal plans): the dynamic
 // scheduler hands out a head's largest items first, so the step ends on its smallest ones.
 // VECATTN_ITEM_ORDER=0 keeps the position order (A/B knob).
-static cudaError_t item_order(AttnParams& ap, int32_t* order, cudaStream_t cs) {
+// Work window (vecattn_replica_t item_begin/item_end): only items [lo, hi) of the flattened
+// bh * n_mt + it order are scheduled, always through an order array.
+static cudaError_t item_order(AttnParams& ap, int32_t* order, cudaStream_t cs, int64_t lo, int64_t hi) {
     static const int mode = [] {  // 0 position order, 1 non-causal only (default), 2 causal too
         const char* e = getenv("VECATTN_ITEM_ORDER");
         return e == nullptr ? 1 : atoi(e);
     }();
+    const bool windowed = lo != 0 || hi != ap.BH * ap.n_mt;
     ap.item_order = nullptr;
-    if ((ap.causal && mode < 2) || mode == 0 || ap.n_mt > va::kLptMaxItems) return cudaSuccess;
+    ap.total_items = hi - lo;
+    if (!windowed && ((ap.causal && mode < 2) || mode == 0 || ap.n_mt > va::kLptMaxItems)) return cudaSuccess;
     ap.item_order = order;
-    return va::launch_lpt_order(ap.wl_len, ap.BH, ap.n_mt, order, cs);
+    if (windowed) ap.die_mode = 0;  // the per-die scheduler walks whole heads
+    const int32_t by_position = mode == 0 || (ap.causal && mode < 2) ? 1 : 0;
+    return va::launch_lpt_order(ap.wl_len, ap.BH, ap.n_mt, lo, hi, by_position, order, cs);
 }
 
 size_t vecattn_sparse_workspace_bytes(const vecattn_problem_t* p, int32_t pq, int64_t nnz_cap) {
@@ -937,7 +943,7 @@ vecattn_status_t vecattn_sparse_fwd(const vecattn_problem_t* p, int32_t pq, cons
     tmark(1, cs);
     cudaError_t e = va::launch_worklist(offsets, indices ? indices : reinterpret_cast<const int32_t*>(wl), wl, wl_len,
                                         ap->BH, ap->Np, ap->n_mt, p->N, pq, nnz_cap, cs);
-    if (e == cudaSuccess) e = item_order(*ap, aw.order, cs);
+    if (e == cudaSuccess) e = item_order(*ap, aw.order, cs, 0, ap->BH * ap->n_mt);
     if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, 2 * sizeof(int), cs);
     tmark(2, cs);
     if (e == cudaSuccess) e = va::launch_attn(*ap, (int)p->D, true, attn_grid(ap->total_items), cs);
@@ -1014,6 +1020,9 @@ static vecattn_status_t forward_impl(const vecattn_problem_t* p, const vecattn_s
     if (rep != nullptr) {
         if (rep->n_peers < 0 || rep->n_peers > 8 || rep->head0 < 0 || rep->head0 + p->Hq > rep->heads_total)
             return VECATTN_ERR_INVALID_ARGUMENT;
+        const int64_t n_items = p->B * p->Hq * ((p->N + 255) / 256);
+        if (rep->item_end > 0 && (rep->item_begin < 0 || rep->item_begin >= rep->item_end || rep->item_end > n_items))
+            return VECATTN_ERR_INVALID_ARGUMENT;
         for (int i = 0; i < rep->n_peers && rep->o_multicast == nullptr; ++i) {
             if (!rep->peer_o[i]) return VECATTN_ERR_INVALID_ARGUMENT;
             if (!aligned16(rep->peer_o[i])) return VECATTN_ERR_SHAPE;
@@ -1035,6 +1044,12 @@ static vecattn_status_t forward_impl(const vecattn_problem_t* p, const vecattn_s
                              !tmap_gather(&ap->tm_v, v, (uint64_t)p->D, (uint64_t)rows_kv)))
         st = VECATTN_ERR_UNSUPPORTED;
     if (st != VECATTN_OK) { delete sp; delete ap; return st; }
+    const int64_t n_items = ap->BH * ap->n_mt;
+    int64_t win_lo = 0, win_hi = n_items;
+    if (rep != nullptr && rep->item_end > 0) {
+        win_lo = rep->item_begin;
+        win_hi = rep->item_end;
+    }
     if (replicate) {
         ap->o_mc = static_cast<__nv_bfloat16*>(rep->o_multicast);
         ap->rep_n = rep->o_multicast ? 0 : rep->n_peers;
@@ -1079,7 +1094,7 @@ static vecattn_status_t forward_impl(const vecattn_problem_t* p, const vecattn_s
     if (e == cudaSuccess)
         e = va::launch_plan(w.bitmask, sp->words_per_row, offsets, d_nnz, nnz_cap, wl, wl_len, sp->BH, sp->Np, p->N,
                             s->pq, p->causal ? 1 : 0, cs);
-    if (e == cudaSuccess) e = item_order(*ap, aw.order, cs);
+    if (e == cudaSuccess) e = item_order(*ap, aw.order, cs, win_lo, win_hi);
     if (e == cudaSuccess) e = cudaMemsetAsync(counter, 0, 2 * sizeof(int), cs);
     tmark(2, cs);
     std::unique_lock<std::mutex> lk;

@@ -146,8 +146,9 @@ struct AttnParams {
     int32_t pq, causal;
     float scale, scale_log2;
     int32_t strict_sync;           // attn_db: wait on every ODONE phase (compute-sanitizer synccheck runs)
-    const int32_t* item_order;     // gather, non-causal: [BH*n_mt] item within head for each scheduler
-                                   // position (per-head longest-first) or null (position order)
+    const int32_t* item_order;     // gather: [total_items] item (bh*n_mt + it) for each scheduler
+                                   // position (per-head longest-first; a work window's items), or
+                                   // null (head-major, position order reversed within a head)
     // output replication (vecattn_forward_replicated): each O row also goes to row
     // ((b*rep_heads + rep_head0 + h)*N + r) of every rep_o[i], or once to o_mc (NVLS multicast)
     __nv_bfloat16* rep_o[8];
@@ -163,10 +164,13 @@ cudaError_t launch_worklist(const int64_t* offsets, const int32_t* indices, uint
                             int64_t BH, int64_t Np, int64_t n_it, int64_t N, int32_t pq, int64_t cap,
                             cudaStream_t st);
 cudaError_t launch_attn(const AttnParams& p, int D, bool gather, int grid, cudaStream_t st);
-// Per-head longest-first order of the attention items by tile-chunk count (compact.cu):
-// order[bh*n_mt + pos] = item within head; one CTA per head, n_mt <= kLptMaxItems.
+// Scheduler order of the attention items inside the work window [lo, hi) of the flattened
+// items (compact.cu): head-major; within a head longest first -- by tile-chunk count
+// or (by_position) by position, reversed.  order[pos] = bh*n_mt + it.  One CTA per head;
+// heads with n_mt > kLptMaxItems keep position order, reversed.
 constexpr int64_t kLptMaxItems = 2048;
-cudaError_t launch_lpt_order(const int32_t* wl_len, int64_t BH, int64_t n_mt, int32_t* order, cudaStream_t st);
+cudaError_t launch_lpt_order(const int32_t* wl_len, int64_t BH, int64_t n_mt, int64_t lo, int64_t hi,
+                             int32_t by_position, int32_t* order, cudaStream_t st);
 // Non-causal sparse attention on CTA pairs (attn_pair.cu, D = 128): grid = 2 x min(items, sms/2).
 int attn_pair_grid(int64_t items, int sms);
 cudaError_t launch_attn_pair(const AttnParams& p, int grid, cudaStream_t st);

@@ -44,7 +44,8 @@ class SelectParams(ctypes.Structure):
 class Replica(ctypes.Structure):
     """vecattn_replica_t (include/vecattn.h): where the fused attention -> all-gather stores O."""
     _fields_ = [("n_peers", ctypes.c_int32), ("peer_o", ctypes.c_void_p * 8), ("o_multicast", ctypes.c_void_p),
-                ("head0", ctypes.c_int64), ("heads_total", ctypes.c_int64)]
+                ("head0", ctypes.c_int64), ("heads_total", ctypes.c_int64), ("item_begin", ctypes.c_int64),
+                ("item_end", ctypes.c_int64)]
 
 
 _lib = None
@@ -415,9 +416,11 @@ def forward_into(q, k, v, cfg: SelectConfig, offsets, indices, cap: int, d_nnz, 
     _check("vecattn_forward", rc)
 
 
-def replica(peer_ptrs=(), multicast_ptr: int = 0, head0: int = 0, heads_total: int = 0) -> Replica:
+def replica(peer_ptrs=(), multicast_ptr: int = 0, head0: int = 0, heads_total: int = 0, item_begin: int = 0,
+            item_end: int = 0) -> Replica:
     """vecattn_replica_t from raw device addresses (e.g. a torch symmetric-memory handle's
-    buffer_ptrs / multicast_ptr) of every rank's full O [B, heads_total, N, D] bf16."""
+    buffer_ptrs / multicast_ptr) of every rank's full O [B, heads_total, N, D] bf16, and an
+    optional work window [item_begin, item_end) over the call's flattened 256-row items."""
     peer_ptrs = [int(x) for x in peer_ptrs]
     if len(peer_ptrs) > 8:
         raise ValueError("vecattn: at most 8 replicas")
@@ -428,6 +431,8 @@ def replica(peer_ptrs=(), multicast_ptr: int = 0, head0: int = 0, heads_total: i
     r.o_multicast = int(multicast_ptr) or None
     r.head0 = int(head0)
     r.heads_total = int(heads_total)
+    r.item_begin = int(item_begin)
+    r.item_end = int(item_end)
     return r
 
 

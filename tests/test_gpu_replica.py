@@ -125,3 +125,70 @@ def test_symmetric_memory_one_rank():
     finally:
         if own:
             dist.destroy_process_group()
+
+
+WIN_CASES = [
+    # kind, B, Hq, Hkv, N, D, pq, causal, selection, window cuts (fractions of all items)
+    ("video", 1, 4, 2, 4096 + 100, 128, 64, False, dict(mode="alg1", alpha=1.0, gk=8192), (0.3, 0.55)),
+    ("video", 2, 3, 1, 3000, 128, 64, True, dict(mode="alg1", alpha=1.0, gk=16), (0.2, 0.71)),
+    ("gauss", 1, 2, 2, 2048 + 64, 64, 128, False, dict(mode="exact", alpha=0.5), (0.5, 0.51)),
+]
+
+
+@pytest.mark.parametrize("case", WIN_CASES, ids=[f"{c[0]}-B{c[1]}-H{c[2]}-N{c[4]}-{'c' if c[7] else 'nc'}"
+                                                 for c in WIN_CASES])
+def test_work_windows_partition_the_items(case):
+    """Flattened (head, block) partition: three calls with work windows that cut
+    heads mid-way fill exactly the rows of their items -- together the full O and LSE, bit for
+    bit -- and leave every other row untouched."""
+    kind, B, Hq, Hkv, N, D, pq, causal, sel, cuts = case
+    dev = torch.device("cuda:0")
+    q, k, v = (t.to(dev) for t in synth.make_inputs(kind, B, Hq, Hkv, N, D, cfg_id=4, device="cpu"))
+    cfg = va.SelectConfig(pq=pq, **sel)
+    o_ref, lse_ref, off_ref, _ = va.forward(q, k, v, cfg, causal=causal)
+    torch.cuda.synchronize()
+    n_mt = (N + 255) // 256
+    T = B * Hq * n_mt
+    b1 = max(1, int(cuts[0] * T))
+    bounds = [0, b1, max(b1 + 1, int(cuts[1] * T)), T]
+    nnz = int(off_ref[-1].item())
+    cap = nnz + 1024
+    offsets = torch.empty_like(off_ref)
+    indices = torch.empty(cap, dtype=torch.int32, device=dev)
+    d_nnz = torch.empty(1, dtype=torch.int64, device=dev)
+    pr = va.problem(q, k, causal)
+    ws = torch.empty(va.forward_workspace_bytes(pr, cfg, cap), dtype=torch.uint8, device=dev)
+    full = torch.full((B, Hq, N, D), -3.5, dtype=torch.bfloat16, device=dev)
+    lse_all = torch.full((B, Hq, N), -9.0, dtype=torch.float32, device=dev)
+    row_item = (torch.arange(B * Hq, device=dev)[:, None] * n_mt + torch.arange(N, device=dev)[None, :] // 256)
+    row_item = row_item.view(B, Hq, N)
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        o_w = torch.full((B, Hq, N, D), 11.0, dtype=torch.bfloat16, device=dev)
+        lse_w = torch.full((B, Hq, N), 5.0, dtype=torch.float32, device=dev)
+        rep = va.replica([full.data_ptr()], 0, 0, Hq, lo, hi)
+        va.forward_replicated_into(q, k, v, cfg, offsets, indices, cap, d_nnz, cap, o_w, lse_w, rep, ws, causal)
+        torch.cuda.synchronize()
+        assert torch.equal(offsets, off_ref)  # the selection covers every row
+        inside = (row_item >= lo) & (row_item < hi)
+        assert torch.equal(o_w[inside], o_ref[inside]) and torch.equal(lse_w[inside], lse_ref[inside])
+        assert bool((o_w[~inside] == 11.0).all()) and bool((lse_w[~inside] == 5.0).all())
+        lse_all[inside] = lse_w[inside]
+    assert torch.equal(full, o_ref) and torch.equal(lse_all, lse_ref)
+
+
+def test_work_window_argument_errors():
+    dev = torch.device("cuda:0")
+    q, k, v = (t.to(dev) for t in synth.make_inputs("gauss", 1, 2, 1, 512, 128, cfg_id=3, device="cpu"))
+    cfg = va.SelectConfig(pq=64, mode="alg1", alpha=1.0, gk=16)
+    pr = va.problem(q, k, False)
+    cap = 2 * 512 * 512
+    offsets = torch.empty(2 * 8 + 1, dtype=torch.int64, device=dev)
+    indices = torch.empty(cap, dtype=torch.int32, device=dev)
+    d_nnz = torch.empty(1, dtype=torch.int64, device=dev)
+    ws = torch.empty(va.forward_workspace_bytes(pr, cfg, cap), dtype=torch.uint8, device=dev)
+    o = torch.empty_like(q)
+    T = 2 * 2
+    for lo, hi in ((2, 2), (3, 1), (-1, 2), (0, T + 1)):
+        with pytest.raises(va.VecAttnError):
+            va.forward_replicated_into(q, k, v, cfg, offsets, indices, cap, d_nnz, cap, o, None,
+                                       va.replica([], 0, 0, 2, lo, hi), ws, False)
