@@ -72,6 +72,10 @@ def parse():
     ap.add_argument("--quick", action="store_true", help="small debug run (no e2e/dense/cpu)")
     ap.add_argument("--no-context", action="store_true", help="skip the torch SDPA / flash-attn dense timings")
     ap.add_argument("--no-causal-extra", action="store_true", help="skip the causal vlm128k extra line")
+    ap.add_argument("--flat-partition", action="store_true",
+                    help="N > 1: split the flattened (head, 256-row item) work evenly over ranks (work windows of "
+                         "vecattn_forward_replicated) instead of whole heads; per-rank selection statistics then "
+                         "count a head shared by two ranks on both")
     ap.add_argument("--nccl-gather", action="store_true",
                     help="N > 1: all-gather O with NCCL after each KV-head group instead of the fused "
                          "symmetric-memory stores of the attention epilogue")
@@ -92,6 +96,17 @@ def head_range(H, ws, rank):
     h0 = rank * base + min(rank, rem)
     return h0, h0 + base + (1 if rank < rem else 0), base + (1 if rem else 0)
 
+
+
+def flat_window(H, N, ws, rank):
+    """Flattened (head, 256-row item) partition of SURVEY 8(e) (B = 1): rank r owns items
+    [r T / ws, (r+1) T / ws) of the T = H * ceil(N/256) items.  Returns the query heads
+    [h0, h1) those items touch and the window relative to head h0's first item (the
+    item_begin / item_end of vecattn_replica_t)."""
+    n_items = (N + 255) // 256
+    lo, hi = rank * H * n_items // ws, (rank + 1) * H * n_items // ws
+    h0, h1 = lo // n_items, -(-hi // n_items)
+    return h0, h1, (lo - h0 * n_items, hi - h0 * n_items)
 
 
 def local_kv(H, Hkv, h0, h1):
@@ -187,12 +202,20 @@ class SymmGather:
     it (every rank's stores have landed) orders the buffers.  `ok` is False (and `why` says
     why) when symmetric memory is unavailable; the bench then uses HeadGather (NCCL)."""
 
-    def __init__(self, H, Hkv, B, N, D, ws, rank, dtype, device, ngroups=4, group=None):
+    def __init__(self, H, Hkv, B, N, D, ws, rank, dtype, device, ngroups=4, group=None, h_range=None, window=None):
         self.H, self.B, self.N, self.D, self.ws, self.rank = H, B, N, D, ws, rank
         # one call over all local heads: there is no all-gather to overlap with later groups,
-        # and one call gives the attention's item scheduler the whole rank's items to balance
-        self.plans = [kv_groups(H, Hkv, ws, r, 1) for r in range(ws)]
-        self.h0 = head_range(H, ws, rank)[0]
+        # and one call gives the attention's item scheduler the whole rank's items to balance.
+        # h_range/window: the rank's heads and item window of the flattened partition.
+        self.window = window
+        if h_range is not None and window is not None:
+            h0, h1 = h_range
+            self.h0 = h0
+            self.plans = [None] * ws
+            self.plans[rank] = [(0, h1 - h0, 0, local_kv(H, Hkv, h0, h1)[0])]
+        else:
+            self.plans = [kv_groups(H, Hkv, ws, r, 1) for r in range(ws)]
+            self.h0 = head_range(H, ws, rank)[0]
         self.ok, self.why, self.mc, self.mode = False, "", 0, "p2p"
         try:
             import torch.distributed as dist
@@ -213,7 +236,8 @@ class SymmGather:
         import paper_2603_29494_b200.vecattn as va
         self.handle.barrier(channel=0)
         for g, rng in enumerate(self.plans[self.rank]):
-            rep = va.replica([] if self.mc else self.peers, self.mc, self.h0 + rng[0], self.H)
+            w = self.window or (0, 0)
+            rep = va.replica([] if self.mc else self.peers, self.mc, self.h0 + rng[0], self.H, w[0], w[1])
             compute(g, rng, rep)
         self.handle.barrier(channel=0)
 
@@ -384,6 +408,13 @@ def run_ours(args):
     B, H, Hkv, N, D, causal = wl.B, wl.Hq, wl.Hkv, wl.N, wl.D, wl.causal
     pq, bk, gk = args.pq, args.bk, (args.gk or wl.gk)
     h0, h1, hmax = head_range(H, ws, rank)
+    window = None
+    if args.flat_partition and ws > 1:
+        # flattened (head, 256-row item) partition: rank r computes items
+        # [r T / ws, (r+1) T / ws) of the B*H*ceil(N/256) items, with the heads they touch
+        # (a head cut between two ranks is selected on both; each computes its own rows)
+        assert B == 1, "--flat-partition: B = 1"
+        h0, h1, window = flat_window(H, N, ws, rank)
     Hl = h1 - h0
 
     q, k, v = build_inputs(wl, args.kind, dev, h0, h1)
@@ -448,11 +479,14 @@ def run_ours(args):
     o = torch.empty_like(q)
     lse = torch.empty(B, Hl, N, dtype=torch.float32, device=dev)
     hg = HeadGather(H, Hkv, B, N, D, ws, rank, torch.bfloat16, dev) if ws > 1 else None
-    sg = SymmGather(H, Hkv, B, N, D, ws, rank, torch.bfloat16, dev) if ws > 1 and not args.nccl_gather else None
+    sg = (SymmGather(H, Hkv, B, N, D, ws, rank, torch.bfloat16, dev, h_range=(h0, h1), window=window)
+          if ws > 1 and not args.nccl_gather else None)
     if sg is not None:
         okt = torch.tensor([1 if sg.ok else 0], dtype=torch.int32, device=dev)
         dist.all_reduce(okt, op=dist.ReduceOp.MIN)  # every rank takes the same all-gather path
         if not int(okt.item()):
+            if window is not None:
+                raise SystemExit(f"--flat-partition needs symmetric memory ({sg.why or 'on another rank'})")
             print(f"[bench] symmetric memory unavailable ({sg.why or 'on another rank'}); NCCL all-gather instead",
                   file=sys.stderr)
             sg = None
@@ -580,7 +614,7 @@ def run_ours(args):
 
     # ---- end-to-end through the C ABI with host buffers (pinned H2D in, O D2H out)
     e2e = None
-    if not args.no_e2e and not args.quick:
+    if not args.no_e2e and not args.quick and window is None:  # (e2e groups are whole heads)
         qh = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
         kh = torch.empty(k.shape, dtype=k.dtype, pin_memory=True)
         vh = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
@@ -721,7 +755,7 @@ def run_ours(args):
                    "pq": pq, "bk": bk, "gk": gk, "mode": args.mode, "alpha": alpha, "rho_target": args.rho,
                    "rho_achieved": round(1.0 - float(sp_tot[0]) / (4.0 * D) /
                                          (H * B * (N * N if not causal else N * (N + 1) / 2)), 5),
-                   "nnz": int(sp_tot[1]), "parallelism": f"head-parallel x{ws}" + (
+                   "nnz": int(sp_tot[1]), "parallelism": ("flattened (head, item)" if window else "head") + f"-parallel x{ws}" + (
                        "" if ws == 1 else (f" + O all-gather fused into the attention epilogue ({sg.mode} stores into symmetric memory)"
                                            if sg is not None else " + NCCL all-gather(O) per KV-head group, overlapped")),
                    "l2": "256 MB L2 flush between timed steps; inputs (2.4 GB) >> L2"},
