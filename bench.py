@@ -633,6 +633,9 @@ def run_ours(args):
         nkv, nq = k.shape[1], q.shape[1]
         rep_l = nq // nkv
         sizes = e2e_groups(nkv) if B == 1 else [nkv]
+        if os.environ.get("BENCH_E2E_GROUPS") and B == 1:  # A/B of the group ramp (sizes summing to nkv)
+            sizes = [int(x) for x in os.environ["BENCH_E2E_GROUPS"].split(",")]
+            assert sum(sizes) == nkv, sizes
         cb = [0]
         for g in sizes:
             cb.append(cb[-1] + g)
