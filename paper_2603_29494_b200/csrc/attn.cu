@@ -60,6 +60,11 @@ constexpr int kChunk = 128;                 // keys per K/V chunk
 constexpr uint32_t kKeyMask = 0x0FFFFFFFu;  // entry = key | membership << 28
 constexpr uint32_t kPad = 0x0FFFFFFFu;      // meta key for padding lanes (sorts last)
 constexpr uint32_t kNegInfBits = 0xff800000u;
+// VA_ATTN_ILP (build knob): shorter dependency chains in the softmax (8 max chains, 4 row-sum
+// chains).  Sums in a different order: results differ from VA_ATTN_ILP=0 in rounding only.
+#ifndef VA_ATTN_ILP
+#define VA_ATTN_ILP 1
+#endif
 #ifndef VA_ATTN_POLY_NUM
 #define VA_ATTN_POLY_NUM 1
 #endif
@@ -512,6 +517,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                 }
                 float mx;
                 {
+#if VA_ATTN_ILP
+                    // 8 independent FMNMX3 chains (8 deep) instead of 4 (16 deep): the row max is
+                    // on the softmax's critical path
+                    float m8[8];
+#pragma unroll
+                    for (int x = 0; x < 8; ++x) m8[x] = -INFINITY;
+#pragma unroll
+                    for (int t = 0; t < 128; t += 16) {
+#pragma unroll
+                        for (int x = 0; x < 8; ++x)
+                            m8[x] = fmaxf(fmaxf(m8[x], __uint_as_float(a[t + 2 * x])), __uint_as_float(a[t + 2 * x + 1]));
+                    }
+                    mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+#else
                     float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
                     for (int t = 0; t < 128; t += 8) {
@@ -521,6 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                         m4[3] = fmaxf(fmaxf(m4[3], __uint_as_float(a[t + 6])), __uint_as_float(a[t + 7]));
                     }
                     mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+#endif
                 }
                 const float m_new = fmaxf(m_ref, mx * sl2);
                 const bool need = m_new > m_ref + 8.0f;
@@ -547,6 +567,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     const float neg_m = (m_ref == -INFINITY) ? 0.f : -m_ref;
                     const uint64_t sl2x2 = pack_f32x2(sl2, sl2);
                     const uint64_t nmx2 = pack_f32x2(neg_m, neg_m);
+#if VA_ATTN_ILP
+                    float2 ls[4] = {lsum2, make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#endif
 #pragma unroll
                     for (int qd = 0; qd < 4; ++qd) {
                         uint32_t pk[16];
@@ -565,12 +588,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                             } else {
                                 p0 = ex2(xa.x), p1 = ex2(xa.y), p2 = ex2(xb.x), p3 = ex2(xb.y);
                             }
+#if VA_ATTN_ILP
+                            ls[qd] = fadd2(ls[qd], fadd2(make_float2(p0, p1), make_float2(p2, p3)));  // 4 chains
+#else
                             lsum2 = fadd2(lsum2, fadd2(make_float2(p0, p1), make_float2(p2, p3)));
+#endif
                             pk[t0 >> 1] = pack_bf16x2(p0, p1);
                             pk[(t0 >> 1) + 1] = pack_bf16x2(p2, p3);
                         }
                         tmem_st16(tS + 16 * qd, pk);
                     }
+#if VA_ATTN_ILP
+                    lsum2 = fadd2(fadd2(ls[0], ls[1]), fadd2(ls[2], ls[3]));
+#endif
                     tmem_st_wait();
                 }
                 tc_fence_before();

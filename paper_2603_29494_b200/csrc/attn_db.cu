@@ -421,7 +421,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                 mma_commit(&bars[C::B_KEMPTY + (int)(c % S_)]);
                 if (I.n_chunks == 1) mma_commit(&bars[C::B_QEMPTY]);
                 for (int j = 0; j < I.n_chunks; ++j, ++c) {
-                    const int s = (int)(c % S_);
                     const bool more = j + 1 < I.n_chunks;
                     int mn = 0;
                     auto issue_next_s = [&]() {
@@ -491,7 +490,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
             float2 lsum2 = make_float2(0.f, 0.f);
             int jt = 0;  // chunks of this item processed by this tile
             for (int j = 0; j < I.n_chunks; ++j, ++c) {
-                const int s = (int)(c % S_);
                 if (!(chunk_info<GATHER>(I, j).mask & (1 << tile))) continue;
                 const int bi = (int)(ct & 1u);
                 const uint32_t tS = tmem_base + lane_off + s_col(tile, bi);
