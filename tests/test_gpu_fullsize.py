@@ -151,3 +151,33 @@ def test_worklist_multi_stripe_beyond_262144_keys(causal):
     err = np.abs(o_s[0, 0].float().cpu().numpy()[rows[ok]] - oo[ok])
     assert err.max() <= ATOL_MAX and err.mean() <= ATOL_MEAN, (err.max(), err.mean())
     assert np.abs(l_s[0, 0].cpu().numpy()[rows[ok]] - ol[ok]).max() <= LSE_ATOL
+
+
+def test_full_size_work_windows_equal_full_call():
+    """dit128k (2 heads, the bench's inputs and alpha): two work windows of
+    vecattn_forward_replicated that cut head 0 mid-way write exactly the full call's O into one
+    replica, with the per-head longest-first order inside each window."""
+    import bench
+    import paper_2603_29494_b200.vecattn as va
+    va.load()
+    wl = synth.WORKLOADS["dit128k"]
+    dev = torch.device("cuda:0")
+    H = 2
+    q, k, v = bench.build_inputs(wl, "video", dev, 0, H)
+    cfg = va.SelectConfig(mode="alg1", pq=64, bk=16, gk=wl.gk, alpha=1.0039)
+    o_ref, lse_ref, off_ref, _ = va.forward(q, k, v, cfg, causal=False)
+    torch.cuda.synchronize()
+    T = H * ((wl.N + 255) // 256)
+    cap = int(off_ref[-1].item()) + 1024
+    offsets = torch.empty_like(off_ref)
+    indices = torch.empty(cap, dtype=torch.int32, device=dev)
+    d_nnz = torch.empty(1, dtype=torch.int64, device=dev)
+    pr = va.problem(q, k, False)
+    ws = torch.empty(va.forward_workspace_bytes(pr, cfg, cap), dtype=torch.uint8, device=dev)
+    full = torch.zeros_like(q)
+    lse = torch.zeros_like(lse_ref)
+    for lo, hi in ((0, 301), (301, T)):
+        va.forward_replicated_into(q, k, v, cfg, offsets, indices, cap, d_nnz, cap, None, lse,
+                                   va.replica([full.data_ptr()], 0, 0, H, lo, hi), ws, False)
+    torch.cuda.synchronize()
+    assert torch.equal(full, o_ref) and torch.equal(lse, lse_ref)
