@@ -51,7 +51,6 @@ namespace {
 // holds its whole 128-column S row; the others drop to 64 (65536 registers in total).
 constexpr int kThreads = 512;
 constexpr int kLoadWarps = 4;
-constexpr int kSoftmaxRegs = 192, kOtherRegs = 64;
 VA_DEV int loader_index(uint32_t w) { return w == 2 ? 0 : w == 3 ? 1 : w == 12 ? 2 : w == 13 ? 3 : -1; }
 VA_DEV void setmaxnreg_inc192() { asm volatile("setmaxnreg.inc.sync.aligned.u32 192;"); }
 VA_DEV void setmaxnreg_dec64() { asm volatile("setmaxnreg.dec.sync.aligned.u32 64;"); }
