@@ -300,10 +300,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                     const int sv = (int)(cc % VS), vround = (int)(cc / VS);
                     if (lane == 0 && vround > 0) mbar_wait(&bars[C::B_VEMPTY + sv], (vround - 1) & 1);
                     if (lane == 0) trace(p, 1, cc);
-                    __syncwarp();
-                    sMeta[sv * kChunk + lane] = ok0 ? key0 : kPad;
-                    sMeta[sv * kChunk + 32 + lane] = ok1 ? key1 : kPad;
-                    __syncwarp();
+                    __syncwarp();  // every lane after lane 0's VEMPTY wait (the V gathers below)
+                    if (p.causal) {  // the causal softmax's per-row prefix search reads the keys
+                        sMeta[sv * kChunk + lane] = ok0 ? key0 : kPad;
+                        sMeta[sv * kChunk + 32 + lane] = ok1 ? key1 : kPad;
+                        __syncwarp();
+                    }
                     if (lane == 0) {
                         // the causal-key hand-off has a waiter only in the causal softmax (an
                         // unobserved arrive is what compute-sanitizer synccheck flags)

@@ -23,9 +23,16 @@ VA_DEV long long globaltimer_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// Compiled in only with -DVA_TRACE=1 (scripts/trace_*.py builds: scripts/build_variant.py
+// <tag> <file> -DVA_TRACE=1); the production kernels carry no timeline code.
+#ifndef VA_TRACE
+#define VA_TRACE 0
+#endif
 VA_DEV void trace(const AttnParams& p, int kind, int64_t c) {
-    if (p.trace != nullptr && blockIdx.x < 2 && c < kTraceChunks)  // CTA 1 (the pair's peer): kinds + 16
-        p.trace[(int64_t)(kind + 16 * blockIdx.x) * kTraceChunks + c] = globaltimer_ns();
+    if constexpr (VA_TRACE != 0) {
+        if (p.trace != nullptr && blockIdx.x < 2 && c < kTraceChunks)  // CTA 1 (the pair's peer): kinds + 16
+            p.trace[(int64_t)(kind + 16 * blockIdx.x) * kTraceChunks + c] = globaltimer_ns();
+    }
 }
 
 // Dynamic item scheduler.  die_mode 0: one atomic counter over the head-major item order.
