@@ -490,17 +490,26 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
             const bool row_ok = qrow < p.N;
             float m_ref = -INFINITY;  // log2-domain reference max (lazy rescaling)
             float2 lsum2 = make_float2(0.f, 0.f);
+            // this tile's chunks only: the shared ones, then its own (no per-chunk plan walk over
+            // the other tile's chunks); a chunk's position in the item (plan::own_chunk) is needed
+            // only for the causal key hand-off, which is indexed by the global chunk counter
+            const int n_own = GATHER ? I.nb + (tile == 0 ? I.n0 : I.n1) : I.n_chunks;
             int jt = 0;  // chunks of this item processed by this tile
-            for (int j = 0; j < I.n_chunks; ++j, ++c) {
-                if (!(chunk_info<GATHER>(I, j).mask & (1 << tile))) continue;
+            for (; jt < n_own;) {
+                int64_t cj = c;
+                if constexpr (GATHER) {
+                    if (p.causal) cj = c + plan::own_chunk(I, tile, jt);
+                } else {
+                    cj = c + jt;
+                }
                 const int bi = (int)(ct & 1u);
                 const uint32_t tS = tmem_base + lane_off + s_col(tile, bi);
                 uint32_t mw[2];
                 if constexpr (GATHER) {
                     mw[0] = mw[1] = 0xffffffffu;  // membership is applied by the MMA
                     if (p.causal) {
-                        mbar_wait(&bars[C::B_MFULL + (int)(c % VS)], (uint32_t)((c / VS) & 1));
-                        const uint32_t* meta = sMeta + (int)(c % VS) * kChunk;
+                        mbar_wait(&bars[C::B_MFULL + (int)(cj % VS)], (uint32_t)((cj / VS) & 1));
+                        const uint32_t* meta = sMeta + (int)(cj % VS) * kChunk;
                         int lo = 0, hi = kChunk;  // keys ascending: visible = prefix with key <= qrow
                         while (lo < hi) {
                             const int mid = (lo + hi) >> 1;
@@ -512,14 +521,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                     }
                 } else {
                     const int64_t vend = p.causal ? min(p.N, qrow + 1) : p.N;
-                    const int64_t nv = vend - (int64_t)j * kChunk;
+                    const int64_t nv = vend - (int64_t)jt * kChunk;
                     mw[0] = prefix_mask(nv);
                     mw[1] = prefix_mask(nv - 32);
                 }
                 const bool full = (mw[0] & mw[1]) == 0xffffffffu;
                 mbar_wait(&bars[C::B_SFULL + 2 * tile + bi], (ct >> 1) & 1u);
                 tc_fence_after();
-                if (lane == 0 && (warp == 2 || warp == 6)) trace(p, 6 + 2 * tile, c);
+                if (lane == 0 && (warp == 2 || warp == 6)) trace(p, 6 + 2 * tile, cj);
                 __syncwarp();  // reconverge after the per-row causal search (tcgen05.ld is .sync.aligned)
                 // ---- single TMEM pass (TMEM reads, 64 B/clk/SM, bind at D = 128): S -> registers,
                 // masked row max, lazy O rescale, P = exp2(s*scale*log2e - m) bf16-packed over S.
@@ -605,10 +614,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                     for (; od < ct; ++od) mbar_wait(&bars[C::B_ODONE + tile], od & 1u);
                 tc_fence_before();
                 mbar_arrive(&bars[C::B_PFULL + 2 * tile + bi]);
-                if (lane == 0 && (warp == 2 || warp == 6)) trace(p, 7 + 2 * tile, c);
+                if (lane == 0 && (warp == 2 || warp == 6)) trace(p, 7 + 2 * tile, cj);
                 ++ct;
                 ++jt;
             }
+            c += I.n_chunks;
             // ---------------------------------------------------------------- epilogue
             // rows that only ever saw masked keys carry m_ref ~ -2^100*scale*log2e: no visible key
             const float l = (m_ref < -0x1p99f * sl2) ? 0.f : lsum2.x + lsum2.y;  // scale-aware: masked = -2^100*sl2

@@ -140,6 +140,14 @@ VA_DEV Chunk chunk_info(const Item& I, int j) {
     }
 }
 
+// Position in the item of tile t's q-th chunk (gather plans): the shared chunks, then its own
+// single-tile chunks -- interleaved with the other tile's, then the longer list's tail.
+VA_DEV int own_chunk(const Item& I, int t, int q) {
+    if (q < I.nb) return q;
+    const int r = q - I.nb, m = min(I.n0, I.n1);
+    return I.nb + (r < m ? 2 * r + t : 2 * m + (r - m));
+}
+
 // First chunk index > j that tile t computes (n_chunks if none).
 template <bool GATHER>
 VA_DEV int next_chunk(const Item& I, int t, int j) {
