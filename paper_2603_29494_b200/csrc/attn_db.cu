@@ -43,6 +43,11 @@ namespace db {
 
 namespace {
 
+// VA_DB_WARP_WAIT (build knob): loader warps wait on their EMPTY barriers with every lane
+// (1) or with lane 0 behind a divergent branch (0).
+#ifndef VA_DB_WARP_WAIT
+#define VA_DB_WARP_WAIT 1
+#endif
 constexpr int kThreads = 448;  // w0 sched+Q, w1 MMA, w2-5 softmax tile 0, w6-9 softmax tile 1, w10-13 loaders
 constexpr int kLoadWarps = 4;
 constexpr int kFirstLoadWarp = 10;
@@ -266,7 +271,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                     const int ra = lo ? a0 : b0_, rb = lo ? a1 : b1_, rc = lo ? a2 : b2_, rd = lo ? a3 : b3_;
                     // ---- K: bias rows, then the gathers
                     if (k_role) {
+#if VA_DB_WARP_WAIT
+                    if (round > 0) mbar_wait(&bars[C::B_KEMPTY + s], (round - 1) & 1);  // all lanes: no divergence
+#else
                     if (lane == 0 && round > 0) mbar_wait(&bars[C::B_KEMPTY + s], (round - 1) & 1);
+#endif
                     if (lane == 0) trace(p, 0, cc);
                     __syncwarp();
                     {
@@ -298,7 +307,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                     // PV(cc - 2 VS) -- the phase before the one waited for -- is complete.
                     if (v_role) {
                     const int sv = (int)(cc % VS), vround = (int)(cc / VS);
+#if VA_DB_WARP_WAIT
+                    if (vround > 0) mbar_wait(&bars[C::B_VEMPTY + sv], (vround - 1) & 1);
+#else
                     if (lane == 0 && vround > 0) mbar_wait(&bars[C::B_VEMPTY + sv], (vround - 1) & 1);
+#endif
                     if (lane == 0) trace(p, 1, cc);
                     __syncwarp();  // every lane after lane 0's VEMPTY wait (the V gathers below)
                     if (p.causal) {  // the causal softmax's per-row prefix search reads the keys
