@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     const bool lo = lane < 8;
                     const int ra = lo ? a0 : b0_, rb = lo ? a1 : b1_, rc = lo ? a2 : b2_, rd = lo ? a3 : b3_;
                     // ---- K: bias rows, then the gathers
-                    if (lane == 0 && round > 0) mbar_wait(&bars[C::B_KEMPTY + s], (round - 1) & 1);
+                    if (round > 0) mbar_wait(&bars[C::B_KEMPTY + s], (round - 1) & 1);  // all lanes: no divergence
                     if (lane == 0 && hh == 0) trace(p, 0, cc);
                     __syncwarp();
                     {
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                                         rd);
                     }
                     // ---- V: keys for the causal mask, then the gathers
-                    if (lane == 0 && round > 0) mbar_wait(&bars[C::B_VEMPTY + s], (round - 1) & 1);
+                    if (round > 0) mbar_wait(&bars[C::B_VEMPTY + s], (round - 1) & 1);
                     if (lane == 0 && hh == 0) trace(p, 1, cc);
                     __syncwarp();
                     sMeta[s * kChunk + kb + lane] = ok0 ? key0 : kPad;
