@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                         fence_proxy_async();  // generic-proxy smem write -> tcgen05.mma (async proxy)
                     }
                     __syncwarp();
-                    if (lane == 0) mbar_arrive_expect_tx(&bars[C::B_KFULL + s], 64 * D * 2);
+                    mbar_arrive_expect_tx_if(&bars[C::B_KFULL + s], 64 * D * 2, lane == 0);
                     if (lane < 16) {
                         uint8_t* dst = sK + s * C::kKVBytes + (kb + 4 * (int)lane) * 128;
 #pragma unroll
@@ -297,10 +297,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_kernel(const __grid_constant
                     sMeta[s * kChunk + kb + lane] = ok0 ? key0 : kPad;
                     sMeta[s * kChunk + kb + 32 + lane] = ok1 ? key1 : kPad;
                     __syncwarp();
-                    if (lane == 0) {
-                        if (p.causal) mbar_arrive(&bars[C::B_MFULL + s]);  // waited by the causal softmax only
-                        mbar_arrive_expect_tx(&bars[C::B_VFULL + s], 64 * D * 2);
-                    }
+                    mbar_arrive_if(&bars[C::B_MFULL + s], lane == 0 && p.causal);  // waited by the causal softmax only
+                    mbar_arrive_expect_tx_if(&bars[C::B_VFULL + s], 64 * D * 2, lane == 0);
                     if (lane < 16) {
                         uint8_t* dst = sV + s * C::kKVBytes + (kb + 4 * (int)lane) * 128;
 #pragma unroll

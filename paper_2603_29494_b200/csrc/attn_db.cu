@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                         fence_proxy_async();  // generic-proxy smem write -> tcgen05.mma (async proxy)
                     }
                     __syncwarp();
-                    if (lane == 0) mbar_arrive_expect_tx(&bars[C::B_KFULL + s], kChunk * D * 2);
+                    mbar_arrive_expect_tx_if(&bars[C::B_KFULL + s], kChunk * D * 2, lane == 0);
                     if (lane < 16) {
                         uint8_t* dst = sK + s * C::kKVBytes + 4 * (int)lane * 128;
 #pragma unroll
@@ -319,12 +319,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
                         sMeta[sv * kChunk + 32 + lane] = ok1 ? key1 : kPad;
                         __syncwarp();
                     }
-                    if (lane == 0) {
-                        // the causal-key hand-off has a waiter only in the causal softmax (an
-                        // unobserved arrive is what compute-sanitizer synccheck flags)
-                        if (p.causal) mbar_arrive(&bars[C::B_MFULL + sv]);
-                        mbar_arrive_expect_tx(&bars[C::B_VFULL + sv], kChunk * D * 2);
-                    }
+                    // the causal-key hand-off has a waiter only in the causal softmax (an
+                    // unobserved arrive is what compute-sanitizer synccheck flags)
+                    mbar_arrive_if(&bars[C::B_MFULL + sv], lane == 0 && p.causal);
+                    mbar_arrive_expect_tx_if(&bars[C::B_VFULL + sv], kChunk * D * 2, lane == 0);
                     if (lane < 16) {
                         uint8_t* dst = sV + sv * C::kKVBytes + 4 * (int)lane * 128;
 #pragma unroll

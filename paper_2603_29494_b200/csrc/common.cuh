@@ -49,6 +49,23 @@ VA_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
                  "r"(bytes)
                  : "memory");
 }
+// Predicated forms for warp-wide code: only lanes with pred != 0 arrive, and the warp does not
+// branch (a single-lane `if` around an arrive costs a divergent branch and reconvergence in
+// the hot loops).
+VA_DEV void mbar_arrive_if(uint64_t* bar, uint32_t pred) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n"
+        " @p mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n}" ::"r"(smem_u32(bar)),
+        "r"(pred)
+        : "memory");
+}
+VA_DEV void mbar_arrive_expect_tx_if(uint64_t* bar, uint32_t bytes, uint32_t pred) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n"
+        " @p mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n}" ::"r"(smem_u32(bar)),
+        "r"(bytes), "r"(pred)
+        : "memory");
+}
 VA_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
