@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
             const Item I = decode_item<GATHER>(p, item);
             if (I.n_chunks == 0) continue;
             if (lane == 0) {
-                if (qi > 0) mbar_wait(&bars[C::B_QEMPTY], (qi - 1) & 1);
+                if (qi > 0) mbar_wait_long(&bars[C::B_QEMPTY], (qi - 1) & 1);  // waits out an item
                 mbar_arrive_expect_tx(&bars[C::B_QFULL], 2 * C::kQTileBytes);
 #pragma unroll
                 for (int t = 0; t < 2; ++t)
@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_db_kernel(const __grid_const
             const float inv = l > 0.f ? 1.f / l : 0.f;
             const plan::ORow orow = plan::o_row<D>(p, I.bh, qrow);
             if (I.n_chunks > 0) {  // every PV of the item complete (ODONE parity may be 2 behind here)
-                mbar_wait(&bars[C::B_OFIN + tile], fi & 1u);
+                mbar_wait_long(&bars[C::B_OFIN + tile], fi & 1u);
                 ++fi;
             }
             if (jt > 0) {

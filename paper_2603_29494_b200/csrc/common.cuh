@@ -77,8 +77,36 @@ VA_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// VA_WAIT_HINT_NS (build knob): suspend-time hint of the try_wait in mbar_wait (0 = the
+// system default).  Without a hint a waiting thread re-polls every few ns, and a warp that waits
+// for long (a scheduler waiting out an item, a softmax waiting for S) spends issue slots its SMSP
+// neighbours need; with one the thread sleeps until the phase completes or the hint expires.
+#ifndef VA_WAIT_HINT_NS
+#define VA_WAIT_HINT_NS 100000
+#endif
+VA_DEV bool mbar_try_wait_hint(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(hint_ns)
+        : "memory");
+    return ok != 0;
+}
 VA_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
-    while (!mbar_try_wait(bar, parity)) {
+    if constexpr (VA_WAIT_HINT_NS > 0) {
+        while (!mbar_try_wait_hint(bar, parity, VA_WAIT_HINT_NS)) {
+        }
+    } else {
+        while (!mbar_try_wait(bar, parity)) {
+        }
+    }
+}
+// Long waits (a warp idling for most of an item): always with a suspend-time hint.
+VA_DEV void mbar_wait_long(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait_hint(bar, parity, 1000000u)) {
     }
 }
 
