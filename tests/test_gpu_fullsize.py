@@ -181,3 +181,31 @@ def test_full_size_work_windows_equal_full_call():
                                    va.replica([full.data_ptr()], 0, 0, H, lo, hi), ws, False)
     torch.cuda.synchronize()
     assert torch.equal(full, o_ref) and torch.equal(lse, lse_ref)
+
+
+def test_item_order_fallback_beyond_2048_items_per_head():
+    """N > 524288 (more than kLptMaxItems = 2048 items per head): the item order falls back to
+    position order inside lpt_order_kernel.  The fused forward still equals the two-call path,
+    and two work windows still tile the full call."""
+    import paper_2603_29494_b200.vecattn as va
+    va.load()
+    dev = torch.device("cuda:0")
+    N, D = 524288 + 300, 64
+    q, k, v = (t.to(dev) for t in synth.make_inputs("gauss", 1, 1, 1, N, D, cfg_id=9, device="cpu"))
+    cfg = va.SelectConfig(mode="alg1", pq=64, gk=16, alpha=0.3)
+    o, lse, off, idx = va.forward(q, k, v, cfg, causal=False)
+    o2, lse2 = va.sparse_fwd(q, k, v, off, idx, pq=64, causal=False)
+    torch.cuda.synchronize()
+    assert torch.equal(o, o2) and torch.equal(lse, lse2)
+    T = (N + 255) // 256
+    cap = int(off[-1].item()) + 1024
+    offsets = torch.empty_like(off)
+    indices = torch.empty(cap, dtype=torch.int32, device=dev)
+    d_nnz = torch.empty(1, dtype=torch.int64, device=dev)
+    ws = torch.empty(va.forward_workspace_bytes(va.problem(q, k, False), cfg, cap), dtype=torch.uint8, device=dev)
+    full = torch.zeros_like(q)
+    for lo, hi in ((0, 777), (777, T)):
+        va.forward_replicated_into(q, k, v, cfg, offsets, indices, cap, d_nnz, cap, None, None,
+                                   va.replica([full.data_ptr()], 0, 0, 1, lo, hi), ws, False)
+    torch.cuda.synchronize()
+    assert torch.equal(full, o)
