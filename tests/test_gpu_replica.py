@@ -192,3 +192,32 @@ def test_work_window_argument_errors():
         with pytest.raises(va.VecAttnError):
             va.forward_replicated_into(q, k, v, cfg, offsets, indices, cap, d_nnz, cap, o, None,
                                        va.replica([], 0, 0, 2, lo, hi), ws, False)
+
+
+def test_item_order_does_not_change_results(tmp_path):
+    """The per-head longest-first item order only changes which SM computes an item: O and LSE
+    equal the position-order run (VECATTN_ITEM_ORDER=0, read once per process, so the
+    reference runs in a subprocess) bit for bit."""
+    import os
+    import subprocess
+    import sys
+    dev = torch.device("cuda:0")
+    args = ("video", 1, 3, 3, 8192 + 77, 128, 64)
+    q, k, v = (t.to(dev) for t in synth.make_inputs(*args[:6], cfg_id=6, device="cpu"))
+    cfg = va.SelectConfig(pq=64, mode="alg1", alpha=1.0, gk=8192)
+    o, lse, _, _ = va.forward(q, k, v, cfg, causal=False)
+    torch.cuda.synchronize()
+    out = tmp_path / "ref.pt"
+    code = (
+        "import torch, sys\n"
+        "from paper_2603_29494_b200 import synth\n"
+        "import paper_2603_29494_b200.vecattn as va\n"
+        f"q, k, v = (t.to('cuda:0') for t in synth.make_inputs(*{args[:6]!r}, cfg_id=6, device='cpu'))\n"
+        "cfg = va.SelectConfig(pq=64, mode='alg1', alpha=1.0, gk=8192)\n"
+        "o, lse, _, _ = va.forward(q, k, v, cfg, causal=False)\n"
+        f"torch.save((o.cpu(), lse.cpu()), {str(out)!r})\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, VECATTN_ITEM_ORDER="0", PYTHONPATH=root)
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, cwd=root, timeout=300)
+    o_ref, lse_ref = torch.load(out)
+    assert torch.equal(o.cpu(), o_ref) and torch.equal(lse.cpu(), lse_ref)
