@@ -48,3 +48,8 @@ print("K issue duration (K_issue->K_issue_end):", st(d(0, 10)))
 print("V issue duration (V_issue->V_issue_end):", st(d(1, 11)))
 print("K issue_end->landed:", st(d(10, 2)))
 print("V issue_end->landed:", st(d(11, 3)))
+# item boundaries: the largest gaps between consecutive S0_ready events
+s0 = np.array([t[6, c] for c in range(n) if t[6, c] > 0])
+g = np.diff(s0)
+print("S0_ready period:", st(g))
+print("largest S0_ready gaps (ns, item boundaries):", np.sort(g)[-8:].tolist())
