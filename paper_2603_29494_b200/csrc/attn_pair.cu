@@ -351,10 +351,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int i = 0; i < 4; ++i) rows[i] = (int)(row0 + (e[i] == 0xFFFFFFFFu ? 0u : (e[i] & kKeyMask)));
                 if (is_k) {
                     // ---- K half: bias rows, then the gathers
-                    if (lane == 0) {
-                        if (round > 0) mbar_wait(&bars[B_KEMPTY + s], (round - 1) & 1);
-                        plan::trace(p, 0, cc);
-                    }
+                    if (round > 0) mbar_wait(&bars[B_KEMPTY + s], (round - 1) & 1);  // all lanes: no divergence
+                    if (lane == 0) plan::trace(p, 0, cc);
                     __syncwarp();
                     if (active) {
                         uint8_t* kx = smem + kOffKx + s * kKxBytes;
@@ -386,7 +384,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     if (lane == 0) plan::trace(p, 10, cc);
                 } else {
                     // ---- V: this CTA's 64 columns of all 128 keys
-                    if (lane == 0 && round > 0) mbar_wait(&bars[B_VEMPTY + s], (round - 1) & 1);
+                    if (round > 0) mbar_wait(&bars[B_VEMPTY + s], (round - 1) & 1);
                     __syncwarp();
                     const uint32_t vfull = vfull_l0 + 8u * (uint32_t)s;
                     if (lane == 0 && leader && k == 0) mbar_arrive_expect_tx(&bars[B_VFULL + s], 2 * kVBytes);
@@ -519,9 +517,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0 && quad == 0) plan::trace(p, 7 + 2 * x, cc);
-                if (lane == 0 && p.trace != nullptr && blockIdx.x < 2 && cc < plan::kTraceChunks)  // debug: last warp
-                    atomicMax(reinterpret_cast<unsigned long long*>(p.trace) + (15 + 16 * blockIdx.x) * plan::kTraceChunks + cc,
-                              (unsigned long long)plan::globaltimer_ns());
+                if constexpr (VA_TRACE != 0) {
+                    if (lane == 0 && p.trace != nullptr && blockIdx.x < 2 && cc < plan::kTraceChunks)  // debug: last warp
+                        atomicMax(reinterpret_cast<unsigned long long*>(p.trace) + (15 + 16 * blockIdx.x) * plan::kTraceChunks + cc,
+                                  (unsigned long long)plan::globaltimer_ns());
+                }
                 if (lane == 0) {
                     if (leader) mbar_arrive(&bars[B_PFULL + x]);
                     else mbar_arrive_cluster_relaxed(pfull_l);
