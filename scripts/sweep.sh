@@ -7,7 +7,7 @@ OUT=gpurun_out/sweep_$TAG.jsonl
 : > $OUT
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 run() {
-  timeout -s KILL 400 python bench.py --no-e2e --no-cpu-baseline --steps 3 --warmup 3 --dense-reps 1 "$@" 2>>gpurun_out/sweep_$TAG.err | tail -1 >> $OUT
+  timeout -s KILL 400 python bench.py --no-e2e --no-cpu-baseline --no-context --no-causal-extra --steps 3 --warmup 3 --dense-reps 1 "$@" 2>>gpurun_out/sweep_$TAG.err | tail -1 >> $OUT
 }
 run --workload dit128k --rho 0.785
 run --workload vlm128k --rho 0.785
