@@ -8,7 +8,7 @@ OUT=gpurun_out/sweep_$TAG.jsonl
 : > $OUT
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 run() {
-  timeout -s KILL 400 python bench.py --no-e2e --no-cpu-baseline --steps 3 --warmup 3 --dense-reps 0 "$@" 2>>gpurun_out/sweep_$TAG.err | tail -1 >> $OUT
+  timeout -s KILL 400 python bench.py --no-e2e --no-cpu-baseline --no-context --no-causal-extra --steps 3 --warmup 3 --dense-reps 0 "$@" 2>>gpurun_out/sweep_$TAG.err | tail -1 >> $OUT
 }
 for wl in dit128k vlm64k; do
   for pq in 64 128; do run --workload $wl --pq $pq; done
